@@ -1,0 +1,378 @@
+"""Benchmark of the time-step hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl reference]
+
+One JSON line on rank 0.  A "step" is one ``Simulation.attempt_step`` (all
+ndim fused sweeps + the fp64 CFL controller) over the workload's grid.
+
+* ``value``: cell-updates/s with the state resident in HBM, each step timed
+  with CUDA events on the launch stream (host controller gaps included),
+  L2 flushed (256 MiB write) between steps, summed over K steps, max over
+  ranks.  Counts accepted steps only, as the reference metric does.
+* ``e2e``: the same metric through the public API from pinned host memory:
+  upload of the initial state, K attempt_step calls (each a D2H of the
+  per-sweep max speeds), download of the final state; wall clock.
+* ``roofline``: the dominant sweep kernel's algorithmic bytes per launch
+  (m states read + m written per cell) / its mean CUDA-event
+  duration, against MEASURED_PEAKS.json ``hbm_gbs``.
+* ``cpu_baseline``: the oracle (C restatement of the reference path, all host
+  threads) on a bounded sample of the same workload.
+* ``--impl reference``: the reference's CPU path (oracle port) timed on the
+  host cores on this workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gcell-updates/s and achieved HBM GB/s vs peak at 1/2/4/8 B200 vs CPU ref"
+UNIT = "Gcell-updates/s"
+# CUDACLAW SW 1000^2 fp64 average step 9.2 ms on a Tesla C2050
+PUBLISHED_SW_FP64 = 1.0e6 / 9.2e-3 / 1e9
+
+WORKLOADS = {
+    # name: (problem, cells, lower, upper, profile, options, bc, limiter, precision, label)
+    "c1": ("acoustics2d", (256, 256), (0, 0), (1, 1), "gaussian_pressure",
+           {"amplitude": 1.0, "width": 0.08}, "reflective", "mc", "double",
+           "C1: 2D acoustics 256x256 radial pressure pulse, MC, fp64"),
+    "c2": ("shallow_water2d", (1024, 1024), (-1, -1), (1, 1), "radial_dam_break", {},
+           "reflective", "mc", "double",
+           "C2: 2D shallow water 1024x1024 radial dam-break, reflective, MC, adaptive CFL dt, fp64"),
+    "c3": ("vc_acoustics3d", (256, 256, 256), (0, 0, 0), (1, 1, 1), "two_material_pulse", {},
+           "reflective", "superbee", "double",
+           "C3: 3D acoustics 256^3 two-material medium, superbee, fp64"),
+    "c4": ("shallow_water2d", (16384, 16384), (-1, -1), (1, 1), "radial_dam_break", {},
+           "reflective", "mc", "double",
+           "C4: 2D shallow water 16384x16384 radial dam-break (1 GPU), fp64"),
+    "c5": ("acoustics3d", (512, 512, 512), (0, 0, 0), (1, 1, 1), "gaussian_pressure",
+           {"width": 0.1}, "periodic", "mc", "double",
+           "C5: 3D acoustics 512^3 per GPU, MC, periodic, fp64"),
+    "c5f32": ("acoustics3d", (512, 512, 512), (0, 0, 0), (1, 1, 1), "gaussian_pressure",
+              {"width": 0.1}, "periodic", "mc", "single",
+              "C5: 3D acoustics 512^3 per GPU, MC, periodic, fp32"),
+    "sw8192": ("shallow_water2d", (8192, 8192), (-1, -1), (1, 1), "radial_dam_break", {},
+               "reflective", "mc", "double",
+               "north-star: 2D shallow water 8192^2 radial dam-break, fp64"),
+    "sw8192f32": ("shallow_water2d", (8192, 8192), (-1, -1), (1, 1), "radial_dam_break", {},
+                  "reflective", "mc", "single",
+                  "north-star: 2D shallow water 8192^2 radial dam-break, fp32"),
+}
+
+
+def build_inputs(name):
+    import paper_1805_08846_b200 as P
+    prob, cells, lower, upper, profile, options, bc, lim, prec, label = WORKLOADS[name]
+    problem = P.get_problem(prob)
+    spec = P.GridSpec(cells, lower, upper, problem.num_states)
+    grid = P.create_grid(spec, P.grid.DTYPES[prec])
+    P.fill_initial(grid, problem.initial_profile(profile, dict(options), spec))
+    params = problem.make_params({})
+    speed = problem.speed_bound(grid, params)
+    bspec = P.BoundarySpec.uniform(P.BoundaryKind(bc), problem.normal_velocity)
+    return dict(P=P, problem=problem, spec=spec, grid=grid, params=params, speed=speed,
+                bspec=bspec, limiter=P.LimiterKind(lim), label=label, dtype=grid.dtype)
+
+
+# ---------------------------------------------------------------------------
+# CPU leg (oracle port of the reference path)
+
+
+def oracle_from_inputs(inp, nthreads):
+    from oracle import oracle as O
+    problem = inp["problem"]
+    pd = {"acoustics": lambda p: {"sound_speed": p.sound_speed, "impedance": p.impedance},
+          "shallow_water": lambda p: {"gravity": p.gravity},
+          "advection": lambda p: {"speed": p.speed},
+          "vc_acoustics": lambda p: {}}[problem.solver_name](inp["params"])
+    sides = [(lo.value, hi.value) for lo, hi in inp["bspec"].sides]
+    return O.OracleSimulation(inp["grid"].data.copy(), inp["spec"].spacing, problem.solver_name,
+                              pd, sides, inp["bspec"].normal_velocity,
+                              limiter=inp["limiter"].value, initial_max_speed=inp["speed"],
+                              nthreads=nthreads)
+
+
+def cpu_rate(inp, budget_s=12.0, max_steps=None, warmup=1):
+    """Oracle throughput on all host threads (bounded sample)."""
+    nthreads = os.cpu_count() or 1
+    sim = oracle_from_inputs(inp, nthreads)
+    for _ in range(warmup):
+        sim.attempt_step()
+    cells = inp["spec"].num_cells
+    acc0 = sim.steps_accepted
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        sim.attempt_step()
+        steps += 1
+        el = time.perf_counter() - t0
+        if (max_steps is not None and steps >= max_steps) or (max_steps is None and el >= budget_s):
+            break
+    el = time.perf_counter() - t0
+    acc = sim.steps_accepted - acc0
+    return cells * acc / el / 1e9, nthreads, steps, el
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._nv = pynvml
+        except Exception:
+            self._nv = None
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+        }
+        while not self._stop.is_set():
+            try:
+                util = nv.nvmlDeviceGetUtilizationRates(self._h).gpu
+                mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                if util > 0:
+                    self.samples.append(mhz)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def stop(self):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=2)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(workload, kernel):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)
+        return d.get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    inp = build_inputs(args.workload)
+    rate, nthreads, steps, el = cpu_rate(inp, max_steps=args.steps, warmup=args.warmup)
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * el / max(steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if inp["dtype"] == np.float64 else "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": inp["label"], "cells": list(inp["spec"].cells)},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "sample": f"{steps} steps of the full workload on {nthreads} threads "
+                                   "(oracle/clawref.c + oracle/oracle.py controller)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def flush_l2(buf):
+    buf.zero_()
+
+
+def run_gpu(args, rank, world):
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+    inp = build_inputs(args.workload)
+    P = inp["P"]
+    sim = P.Simulation(inp["grid"], inp["problem"].solver, inp["params"], inp["bspec"],
+                       limiter=inp["limiter"], initial_max_speed=inp["speed"], device=local)
+    dev = sim.device_grid
+    stream = torch.cuda.current_stream()
+    dev.set_stream(stream.cuda_stream)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    ndim = inp["spec"].ndim
+    m = inp["spec"].num_states
+    isz = inp["dtype"].itemsize
+    cells = inp["spec"].num_cells
+
+    for _ in range(args.warmup):
+        sim.attempt_step()
+    dev.timing()  # drain
+    dev.enable_timing(True)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    sampler = ClockSampler(local).start()
+    total_ms = 0.0
+    acc0, rev0 = sim.steps_accepted, sim.steps_reverted
+    for _ in range(args.steps):
+        flush_l2(flush)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sim.attempt_step()
+        e1.record(stream)
+        e1.synchronize()
+        total_ms += e0.elapsed_time(e1)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    acc = sim.steps_accepted - acc0
+    rev = sim.steps_reverted - rev0
+    ms_axis, n_axis = dev.timing()
+    dev.enable_timing(False)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * cells * acc / (total_ms / 1e3) / 1e9
+
+    # roofline: dominant kernel (largest total time)
+    dom = max(range(ndim), key=lambda a: ms_axis[a])
+    bytes_per_launch = cells * m * 2 * isz
+    mean_ms = ms_axis[dom] / max(n_axis[dom], 1)
+    achieved = bytes_per_launch / (mean_ms / 1e3) / 1e9
+    peak, peak_kind = measured_peaks()
+    kname = "sweep_contig" if dom == 0 else "sweep_strided"
+    traffic = ncu_traffic(args.workload, f"axis{dom}")
+    sim.close()
+
+    # e2e through the public API with pinned host buffers
+    from paper_1805_08846_b200._native import PinnedBuffer
+    pin_in = PinnedBuffer(inp["grid"].interior().shape, inp["dtype"])
+    pin_in.array[...] = inp["grid"].interior()
+    pin_out = PinnedBuffer(inp["grid"].interior().shape, inp["dtype"])
+    sim2 = P.Simulation(inp["grid"], inp["problem"].solver, inp["params"], inp["bspec"],
+                        limiter=inp["limiter"], initial_max_speed=inp["speed"], device=local)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    sim2.device_grid.upload(sim2._cur, pin_in.array)
+    a0 = sim2.steps_accepted
+    for _ in range(args.steps):
+        sim2.attempt_step()
+    sim2.device_grid.download(sim2._cur, pin_out.array)
+    e2e_s = time.perf_counter() - t0
+    e2e_acc = sim2.steps_accepted - a0
+    sim2.close()
+    if dist:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    state_bytes = inp["grid"].interior().nbytes
+    e2e = {"value": world * cells * e2e_acc / e2e_s / 1e9, "unit": UNIT,
+           "h2d_bytes_per_step": int(state_bytes / args.steps + 8),
+           "d2h_bytes_per_step": int(state_bytes / args.steps + 12 * ndim)}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        rate, nthreads, steps, el = cpu_rate(inp, budget_s=args.cpu_budget)
+        cpu = {"value": rate, "unit": UNIT, "cores": nthreads, "kind": "port",
+               "sample": f"{steps} steps of the same {inp['label'].split(':')[0]} grid in "
+                         f"{el:.1f} s on {nthreads} host threads (oracle/clawref.c)"}
+    is_sw64 = inp["problem"].solver_name == "shallow_water" and inp["dtype"] == np.float64
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": (value / PUBLISHED_SW_FP64) if is_sw64 else None,
+        "dtype": "f64" if inp["dtype"] == np.float64 else "f32", "data": "synthetic",
+        "config": {"workload": inp["label"], "cells": list(inp["spec"].cells),
+                   "steps_accepted": acc, "steps_reverted": rev,
+                   "l2": "flushed between steps (256 MiB write, untimed)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "vs_baseline_ref": "CUDACLAW SW 1000^2 fp64 9.2 ms/step, C2050 (BASELINE.md)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": f"{kname} (axis {dom})",
+                     "bytes_per_launch": bytes_per_launch, "mean_launch_ms": mean_ms,
+                     "peak_kind": peak_kind,
+                     "per_axis_ms_mean": [ms_axis[a] / max(n_axis[a], 1) for a in range(ndim)]},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(sum(n_axis)),
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_gpu(args, rank, world)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

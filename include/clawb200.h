@@ -1,0 +1,172 @@
+/* clawb200.h -- C ABI of the B200-native time-step hot path.
+ *
+ * The reference (clawtile, /root/reference/pkg) has no C ABI: its hot path is
+ * the Python operator API below, with numba kernels underneath.
+ * specifies a bindings layer ("create/destroy session, evolve, copy-state-out,
+ * last-error string") that was never built; this header is
+ * that layer, one entry point per reference operation it replaces:
+ *
+ *   clb_create / clb_destroy   Simulation.__init__ / close          timestep.py:75-132
+ *                              (+ StateGrid allocation, grid.py:145-160)
+ *   clb_upload / clb_download  fill_initial / StateGrid.interior,   grid.py:174-234
+ *                              frame payload order (frames.py:84-99)
+ *   clb_sweep                  sweep_axis / sweep_axis_tiled        sweep.py:307-391
+ *                              (+ apply_boundary fused, boundary.py:87-122)
+ *   clb_sweep_async/clb_fetch  the same, split for multi-GPU halo exchange
+ *   clb_attempt_step           the sweep loop of Simulation.attempt_step
+ *                              (timestep.py:195-211); the fp64 accept/revert
+ *                              arithmetic stays on the host (timestep.py:212-239)
+ *   clb_first_nonfinite        Simulation._check_finite             timestep.py:179-186
+ *   clb_solve_pairs            RiemannSolver.solve                  riemann.py:205-223
+ *   clb_last_error             (exceptions never cross the ABI)
+ *
+ * Conventions: every function returns 0 on success and a negative CLB_E*
+ * code on failure; clb_last_error(h) (or clb_last_error(NULL) for creation
+ * failures) describes it.  One host thread per handle.  Buffers are device-
+ * resident padded SoA arrays owned by the handle (3 per handle: the current
+ * state plus two sweep scratch buffers, as timestep.py:113).
+ */
+#ifndef CLAWB200_H
+#define CLAWB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Riemann solver ids (riemann.py:256-284 registry names). */
+#define CLB_SOLVER_ADVECTION 0     /* "advection"     m=1               */
+#define CLB_SOLVER_ACOUSTICS 1     /* "acoustics"     m=ndim+1          */
+#define CLB_SOLVER_SHALLOW_WATER 2 /* "shallow_water" m=3, ndim=2       */
+#define CLB_SOLVER_VC_ACOUSTICS 3  /* "vc_acoustics"  m=ndim+3 (p,u..,Z,c) builder extension */
+
+/* Limiter ids: limiter.py:33-39 LIMITER_IDS (stable). */
+#define CLB_LIMITER_NONE 0
+#define CLB_LIMITER_MINMOD 1
+#define CLB_LIMITER_SUPERBEE 2
+#define CLB_LIMITER_MC 3
+#define CLB_LIMITER_VANLEER 4
+
+/* Boundary kinds (boundary.py:20-23) plus HALO: ghost layers read from
+ * memory as-is (a neighbouring rank's halo, or caller-filled ghosts). */
+#define CLB_BC_OUTFLOW 0
+#define CLB_BC_REFLECTIVE 1
+#define CLB_BC_PERIODIC 2
+#define CLB_BC_HALO 3
+
+/* Error codes. */
+#define CLB_OK 0
+#define CLB_EINVAL -1     /* ValueError in the reference */
+#define CLB_ECUDA -2      /* CUDA runtime failure        */
+#define CLB_ENOMEM -3
+#define CLB_EUNSUPPORTED -4
+
+typedef struct clb_ctx *clb_handle;
+
+typedef struct clb_desc {
+    int32_t ndim;               /* 1..3                                            */
+    int32_t num_states;         /* m                                               */
+    int32_t itemsize;           /* 4 (float32) | 8 (float64)                       */
+    int32_t solver_id;          /* CLB_SOLVER_*                                    */
+    int32_t limiter_id;         /* CLB_LIMITER_*                                   */
+    int32_t device;             /* CUDA device ordinal                             */
+    int64_t cells[3];           /* interior cells per logical axis (x, y, z)       */
+    double spacing[3];          /* GridSpec.spacing, fp64 (grid.py:62-66)          */
+    double params[8];           /* solver params packed IN THE RUN DTYPE exactly as
+                                   RiemannSolver.pack_params (riemann.py:235-253),
+                                   then widened to double (exact)                  */
+    int32_t bc[3][2];           /* per axis (lo, hi): CLB_BC_*                     */
+    int32_t normal_velocity[3]; /* BoundarySpec.normal_velocity; -1 = None         */
+} clb_desc;
+
+/* Lifecycle. */
+int clb_create(const clb_desc *desc, clb_handle *out);
+int clb_destroy(clb_handle h);
+const char *clb_last_error(clb_handle h);
+int clb_version(void);
+
+/* Optional: run on a caller-owned cudaStream_t (e.g. torch's current stream
+ * for NCCL ordering).  NULL restores the handle's own stream. */
+int clb_set_stream(clb_handle h, void *cuda_stream);
+
+/* Segment length (cells along the sweep axis per warp/thread) for one
+ * axis; 0 = automatic.  Results are bitwise independent of it (segments
+ * recompute their shared fans, sweep.py:11-16); exposed for tests/tuning. */
+int clb_set_segments(clb_handle h, int axis, int seg_len);
+
+/* Interior transfer, frame-payload order: state-major, then z, y, x (x
+ * fastest), ghost cells excluded; nbytes must equal m*prod(cells)*itemsize.
+ * buf in {0,1,2}. */
+int clb_upload(clb_handle h, int buf, const void *interior, size_t nbytes);
+int clb_download(clb_handle h, int buf, void *interior, size_t nbytes);
+
+/* Whole padded arrays, exactly the reference StateGrid.data layout
+ * (m, [nz+4,] [ny+4,] nx+4), ghosts included (grid.py:145-160).  Used by the
+ * per-sweep API, whose ghost cells are caller-filled and read as-is with
+ * CLB_BC_HALO on the swept axis (sweep.py:206-212). */
+int clb_upload_padded(clb_handle h, int buf, const void *padded, size_t nbytes);
+int clb_download_padded(clb_handle h, int buf, void *padded, size_t nbytes);
+
+/* Change the boundary kinds of one axis after creation (CLB_BC_*). */
+int clb_set_boundary(clb_handle h, int axis, int lo, int hi);
+
+/* One directional sweep src -> dst (src != dst), BCs fused.  dt > 0 (fp64);
+ * dtdx = T(dt / spacing[axis]) is formed exactly as sweep.py:336-337.
+ * Outputs: max |s| over every interface solved (widened to double) and a
+ * non-finite flag for the dst interior.  Synchronous. */
+int clb_sweep(clb_handle h, int axis, double dt, int src, int dst,
+              double *max_abs_speed, int32_t *nonfinite);
+
+/* Asynchronous form: results accumulate in result slot `slot` (0..3) until
+ * clb_fetch.  `literal`=1 selects the fully literal kernel (no structural-
+ * zero elision; used on the blow-up slow path). */
+int clb_sweep_async(clb_handle h, int axis, double dt, int src, int dst, int slot,
+                    int literal);
+int clb_fetch(clb_handle h, int nslots, double *max_abs_speed, int32_t *nonfinite);
+
+/* All ndim sweeps of one step attempt, x then y then z (timestep.py:35-42,
+ * 200-211): sweep j reads the previous output and writes scratch[j % 2].
+ * One device->host read at the end.  speeds[j], nonfinite[j] per sweep. */
+int clb_attempt_step(clb_handle h, double dt, int src, int scratch0, int scratch1,
+                     double *speeds, int32_t *nonfinite);
+
+/* First non-finite interior value of `buf` in C order (state, z, y, x);
+ * found=0 when the buffer is finite.  cell[] is logical (x, y, z). */
+int clb_first_nonfinite(clb_handle h, int buf, int32_t *found, int32_t *state,
+                        int64_t cell[3]);
+
+/* Device pointers for halo exchange along the slowest axis (ndim >= 2):
+ * for side 0 (lo) / 1 (hi) returns the first byte of the 2 owned boundary
+ * rows/planes to SEND and of the 2 ghost rows/planes to RECEIVE into, for
+ * state 0; state k is at + k*state_stride_bytes; each block is
+ * block_bytes long and contiguous (whole pitched rows/planes, ghost
+ * columns included). */
+int clb_halo_layout(clb_handle h, int buf, int side, void **send_ptr, void **recv_ptr,
+                    size_t *block_bytes, size_t *state_stride_bytes);
+
+/* Per-interface solve of n (q_l, q_r) pairs on the device (parity unit for
+ * the Riemann plugins).  q arrays are (n, m) row-major in the run dtype;
+ * W out (n, nw, m), s out (n, nw). */
+int clb_solve_pairs(clb_handle h, int axis, int64_t n, const void *ql, const void *qr,
+                    void *W, void *s);
+
+/* Kernel timing (CUDA events on the launch stream) for the bench: when
+ * enabled, every sweep launch is bracketed by events; clb_timing returns
+ * the summed milliseconds and launch counts per axis and resets them. */
+int clb_enable_timing(clb_handle h, int on);
+int clb_timing(clb_handle h, double ms_per_axis[3], int64_t launches_per_axis[3]);
+
+/* Pinned host memory for end-to-end transfers. */
+void *clb_host_alloc(size_t nbytes);
+void clb_host_free(void *p);
+
+/* Device bytes owned by the handle and the pitch (elements) of one row. */
+int clb_memory_info(clb_handle h, size_t *device_bytes, int64_t *row_pitch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CLAWB200_H */

@@ -1,0 +1,591 @@
+// clb_capi.cu -- the C ABI (include/clawb200.h) over the sm_100a sweep kernels.
+//
+// Device layout (per buffer): m states, each a pitched array shaped like the
+// reference's padded StateGrid (grid.py:145-160) -- two ghost layers on every
+// axis -- but with rows padded to a 128-byte pitch and the interior origin
+// 128-byte aligned:
+//   1-D: [px]     2-D: [ny+4][px]     3-D: [nz+4][ny+4][px]
+// with interior x at columns xoff .. xoff+nx-1 (xoff = 128 B / itemsize).
+// Ghost layers in memory are read only for CLB_BC_HALO sides (a neighbour
+// rank's halo, or the caller-filled ghosts of the per-sweep API, which the
+// reference reads as-is, sweep.py:206-212); physical boundaries are
+// synthesised by the kernels at load time (boundary.py semantics).  Three
+// buffers per handle mirror the reference's grid + two scratch buffers
+// (timestep.py:113).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/clawb200.h"
+#include "clb_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Result {
+  unsigned long long smax[4];
+  int nonfinite[4];
+  unsigned long long first_bad;
+};
+
+struct TimedLaunch {
+  int axis;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct clb_ctx {
+  clb_desc d;
+  int M = 0, ndim = 0, itemsize = 0;
+  int64_t cells[3] = {1, 1, 1};
+  int64_t px = 0, sstride = 0, origin = 0, ystride = 0, zstride = 0;
+  int64_t xoff = 0, ypad = 1, zpad = 1;
+  size_t buf_bytes = 0;
+  void* buf[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  Result* d_res = nullptr;
+  Result* h_res = nullptr;
+  int num_sms = 148;
+  int seg_override[3] = {0, 0, 0};
+  bool timing = false;
+  std::vector<TimedLaunch> launches;
+  std::vector<cudaEvent_t> event_pool;
+  std::string err;
+};
+
+namespace {
+
+int fail(clb_ctx* h, int code, const std::string& msg) {
+  if (h) h->err = msg; else g_create_error = msg;
+  return code;
+}
+
+int cuda_fail(clb_ctx* h, cudaError_t e, const char* where) {
+  return fail(h, CLB_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CLB_CUDA(h, call)                                   \
+  do {                                                      \
+    cudaError_t e_ = (call);                                \
+    if (e_ != cudaSuccess) return cuda_fail((h), e_, #call); \
+  } while (0)
+
+int expected_states(int solver, int ndim) {
+  switch (solver) {
+    case CLB_SOLVER_ADVECTION: return 1;
+    case CLB_SOLVER_ACOUSTICS: return ndim + 1;
+    case CLB_SOLVER_SHALLOW_WATER: return ndim == 2 ? 3 : -1;
+    case CLB_SOLVER_VC_ACOUSTICS: return ndim + 3;
+  }
+  return -1;
+}
+
+cudaEvent_t take_event(clb_ctx* h) {
+  if (!h->event_pool.empty()) {
+    cudaEvent_t e = h->event_pool.back();
+    h->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Geometry of one sweep: which kernel, extents and strides.
+clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
+  clb::GenericArgs g;
+  std::memset(&g, 0, sizeof(g));
+  const int64_t isz = h->itemsize;
+  g.qin = (const char*)h->buf[src] + h->origin * isz;
+  g.qout = (char*)h->buf[dst] + h->origin * isz;
+  g.sstride = h->sstride;
+  g.bc_lo = h->d.bc[axis][0];
+  g.bc_hi = h->d.bc[axis][1];
+  g.nv = h->d.normal_velocity[axis];
+  g.lim_id = h->d.limiter_id;
+  g.num_sms = h->num_sms;
+  const int64_t nx = h->cells[0], ny = h->cells[1], nz = h->cells[2];
+  if (axis == 0) {
+    g.contig = 1;
+    g.n = (int)nx; g.n1 = (int)ny; g.n2 = (int)nz;
+    g.astride = 1; g.t1stride = h->ystride; g.t2stride = h->zstride;
+    const int64_t rows = ny * nz;
+    const int64_t target_warps = (int64_t)h->num_sms * 32;
+    int64_t nseg = (target_warps + rows - 1) / rows;
+    nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, nx / 64));
+    int64_t L = (nx + nseg - 1) / nseg;
+    if (h->seg_override[0] > 0) L = h->seg_override[0];
+    g.seg_len = (int)L;
+    g.nseg = (int)((nx + L - 1) / L);
+    g.block = 128;
+  } else {
+    g.contig = 0;
+    g.n1 = (int)nx;
+    g.t1stride = 1;
+    if (axis == 1) {
+      g.n = (int)ny; g.n2 = (int)nz; g.astride = h->ystride; g.t2stride = h->zstride;
+    } else {
+      g.n = (int)nz; g.n2 = (int)ny; g.astride = h->zstride; g.t2stride = h->ystride;
+    }
+    const int64_t cols = nx * (int64_t)g.n2;
+    const int64_t target_threads = (int64_t)h->num_sms * 2048;
+    int64_t nseg = (target_threads + cols - 1) / cols;
+    nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, g.n / 32));
+    int64_t L = (g.n + nseg - 1) / nseg;
+    if (h->seg_override[axis] > 0) L = h->seg_override[axis];
+    g.seg_len = (int)L;
+    g.nseg = (int)((g.n + L - 1) / L);
+    g.block = nx >= 128 ? 128 : (nx >= 64 ? 64 : 32);
+  }
+  return g;
+}
+
+int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bool literal) {
+  if (axis < 0 || axis >= h->ndim) return fail(h, CLB_EINVAL, "sweep axis out of range");
+  if (src < 0 || src > 2 || dst < 0 || dst > 2) return fail(h, CLB_EINVAL, "buffer index out of range");
+  if (src == dst) return fail(h, CLB_EINVAL, "sweep cannot run in place");
+  if (!(dt > 0.0)) return fail(h, CLB_EINVAL, "dt must be positive");
+  if (slot < 0 || slot > 3) return fail(h, CLB_EINVAL, "result slot out of range");
+  clb::GenericArgs g = sweep_geometry(h, axis, src, dst);
+  // sweep.py:336-337: dtdx = T(dt / dx[axis]) -- fp64 divide, then round to T.
+  const double dtdx64 = dt / h->d.spacing[axis];
+  g.dtdx = h->itemsize == 8 ? dtdx64 : (double)(float)dtdx64;
+  for (int i = 0; i < 4; ++i) g.params[i] = h->d.params[i];
+  g.smax_bits = &h->d_res->smax[slot];
+  g.nonfinite = &h->d_res->nonfinite[slot];
+  TimedLaunch tl{axis, nullptr, nullptr};
+  if (h->timing) {
+    tl.a = take_event(h);
+    tl.b = take_event(h);
+    cudaEventRecord(tl.a, h->stream);
+  }
+  cudaError_t e;
+  switch (h->d.solver_id) {
+    case CLB_SOLVER_ACOUSTICS: e = clb::launch_acoustics(h->itemsize, h->ndim, axis, literal, g, h->stream); break;
+    case CLB_SOLVER_SHALLOW_WATER: e = clb::launch_shallow_water(h->itemsize, h->ndim, axis, literal, g, h->stream); break;
+    case CLB_SOLVER_ADVECTION: e = clb::launch_advection(h->itemsize, h->ndim, axis, literal, g, h->stream); break;
+    default: e = clb::launch_vc_acoustics(h->itemsize, h->ndim, axis, literal, g, h->stream); break;
+  }
+  if (e != cudaSuccess) return cuda_fail(h, e, "sweep launch");
+  if (h->timing) {
+    cudaEventRecord(tl.b, h->stream);
+    h->launches.push_back(tl);
+  }
+  return CLB_OK;
+}
+
+int fetch(clb_ctx* h, int nslots, double* speeds, int32_t* nonfinite) {
+  CLB_CUDA(h, cudaMemcpyAsync(h->h_res, h->d_res, sizeof(Result), cudaMemcpyDeviceToHost, h->stream));
+  CLB_CUDA(h, cudaMemsetAsync(h->d_res, 0, sizeof(Result), h->stream));
+  CLB_CUDA(h, cudaStreamSynchronize(h->stream));
+  for (int i = 0; i < nslots && i < 4; ++i) {
+    if (speeds) {
+      double v;
+      std::memcpy(&v, &h->h_res->smax[i], sizeof(double));
+      speeds[i] = v;
+    }
+    if (nonfinite) nonfinite[i] = h->h_res->nonfinite[i] ? 1 : 0;
+  }
+  return CLB_OK;
+}
+
+// timestep.py:179-186: first non-finite interior value in C order.
+template <typename T>
+__global__ void first_bad_kernel(const T* q, int64_t sstride, int64_t ystride, int64_t zstride,
+                                 int64_t nx, int64_t ny, int64_t nz, int m,
+                                 unsigned long long* out) {
+  const int64_t total = (int64_t)m * nz * ny * nx;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i;
+    const int64_t x = r % nx; r /= nx;
+    const int64_t y = r % ny; r /= ny;
+    const int64_t z = r % nz; r /= nz;
+    const int64_t k = r;
+    const T v = q[k * sstride + z * zstride + y * ystride + x];
+    if (clb::finite_key(v) == 0u) atomicMin(out, (unsigned long long)i);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int clb_version(void) { return 1; }
+
+const char* clb_last_error(clb_handle h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+int clb_create(const clb_desc* desc, clb_handle* out) {
+  if (!desc || !out) return fail(nullptr, CLB_EINVAL, "null argument");
+  *out = nullptr;
+  const clb_desc& d = *desc;
+  if (d.ndim < 1 || d.ndim > 3) return fail(nullptr, CLB_EINVAL, "grid must be 1-, 2- or 3-dimensional");
+  if (d.itemsize != 4 && d.itemsize != 8) return fail(nullptr, CLB_EINVAL, "itemsize must be 4 or 8");
+  if (d.limiter_id < 0 || d.limiter_id > 4) return fail(nullptr, CLB_EINVAL, "unknown limiter id");
+  const int em = expected_states(d.solver_id, d.ndim);
+  if (em < 0) return fail(nullptr, CLB_EUNSUPPORTED, "solver not supported for this dimensionality");
+  if (d.num_states != em)
+    return fail(nullptr, CLB_EUNSUPPORTED, "num_states does not match the device solver's state layout");
+  for (int ax = 0; ax < d.ndim; ++ax) {
+    if (d.cells[ax] < 1 || d.cells[ax] > (int64_t)1 << 30)
+      return fail(nullptr, CLB_EINVAL, "cell counts must be in [1, 2^30]");
+    if (!(d.spacing[ax] > 0.0)) return fail(nullptr, CLB_EINVAL, "spacing must be positive");
+    for (int s = 0; s < 2; ++s) {
+      const int bc = d.bc[ax][s];
+      if (bc < 0 || bc > 3) return fail(nullptr, CLB_EINVAL, "unknown boundary kind");
+      if ((bc == CLB_BC_PERIODIC || bc == CLB_BC_REFLECTIVE) && d.cells[ax] < 2)
+        return fail(nullptr, CLB_EUNSUPPORTED,
+                    "periodic/reflective boundaries need at least 2 cells on the axis");
+      if (bc == CLB_BC_REFLECTIVE &&
+          (d.normal_velocity[ax] < 0 || d.normal_velocity[ax] >= d.num_states))
+        return fail(nullptr, CLB_EINVAL, "reflective boundary needs a normal velocity state");
+    }
+    if ((d.bc[ax][0] == CLB_BC_PERIODIC) != (d.bc[ax][1] == CLB_BC_PERIODIC))
+      return fail(nullptr, CLB_EINVAL, "periodic boundary must be set on both sides");
+  }
+  if (d.solver_id == CLB_SOLVER_ACOUSTICS && !(std::isfinite(d.params[0]) && d.params[0] > 0.0))
+    return fail(nullptr, CLB_EINVAL, "sound speed must be positive and finite");
+
+  clb_ctx* h = new clb_ctx();
+  h->d = d;
+  h->ndim = d.ndim;
+  h->M = d.num_states;
+  h->itemsize = d.itemsize;
+  for (int ax = 0; ax < d.ndim; ++ax) h->cells[ax] = d.cells[ax];
+  const int64_t align = 128 / d.itemsize;
+  h->xoff = align;
+  h->px = (h->xoff + h->cells[0] + 2 + align - 1) / align * align;
+  h->ypad = d.ndim >= 2 ? h->cells[1] + 4 : 1;
+  h->zpad = d.ndim == 3 ? h->cells[2] + 4 : 1;
+  h->ystride = h->px;
+  h->zstride = h->px * h->ypad;
+  h->sstride = h->zstride * h->zpad;
+  h->origin = h->xoff + (d.ndim >= 2 ? 2 * h->ystride : 0) + (d.ndim == 3 ? 2 * h->zstride : 0);
+  h->buf_bytes = (size_t)h->sstride * h->M * h->itemsize;
+
+  cudaError_t e = cudaSetDevice(d.device);
+  if (e != cudaSuccess) { int r = cuda_fail(nullptr, e, "cudaSetDevice"); delete h; return r; }
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, d.device);
+  e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { int r = cuda_fail(nullptr, e, "cudaStreamCreate"); delete h; return r; }
+  h->stream = h->own_stream;
+  for (int i = 0; i < 3; ++i) {
+    e = cudaMalloc(&h->buf[i], h->buf_bytes);
+    if (e != cudaSuccess) {
+      int r = fail(nullptr, CLB_ENOMEM, std::string("device allocation failed: ") + cudaGetErrorString(e));
+      clb_destroy(h);
+      return r;
+    }
+    cudaMemsetAsync(h->buf[i], 0, h->buf_bytes, h->stream);
+  }
+  e = cudaMalloc(&h->d_res, sizeof(Result));
+  if (e == cudaSuccess) e = cudaMallocHost(&h->h_res, sizeof(Result));
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->d_res, 0, sizeof(Result), h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) {
+    int r = cuda_fail(nullptr, e, "result buffers");
+    clb_destroy(h);
+    return r;
+  }
+  *out = h;
+  return CLB_OK;
+}
+
+int clb_destroy(clb_handle h) {
+  if (!h) return CLB_OK;
+  cudaSetDevice(h->d.device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (auto& tl : h->launches) { cudaEventDestroy(tl.a); cudaEventDestroy(tl.b); }
+  for (auto e : h->event_pool) cudaEventDestroy(e);
+  for (int i = 0; i < 3; ++i)
+    if (h->buf[i]) cudaFree(h->buf[i]);
+  if (h->d_res) cudaFree(h->d_res);
+  if (h->h_res) cudaFreeHost(h->h_res);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+  return CLB_OK;
+}
+
+int clb_set_stream(clb_handle h, void* s) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  h->stream = s ? (cudaStream_t)s : h->own_stream;
+  return CLB_OK;
+}
+
+int clb_set_segments(clb_handle h, int axis, int seg_len) {
+  if (!h || axis < 0 || axis > 2 || seg_len < 0) return fail(h, CLB_EINVAL, "bad segment override");
+  h->seg_override[axis] = seg_len;
+  return CLB_OK;
+}
+
+// Pitched 3-D copy of one state between host (dense) and device (pitched).
+static cudaError_t copy_state(clb_ctx* h, int buf, int k, void* host, bool padded, bool to_dev) {
+  const int64_t isz = h->itemsize;
+  const int64_t g = padded ? 2 : 0;
+  const int64_t wx = h->cells[0] + 2 * g;
+  const int64_t wy = h->ndim >= 2 ? h->cells[1] + 2 * g : 1;
+  const int64_t wz = h->ndim == 3 ? h->cells[2] + 2 * g : 1;
+  // device element offset of the copied box's first element
+  int64_t off = (int64_t)k * h->sstride + h->origin - g;
+  if (h->ndim >= 2) off -= g * h->ystride;
+  if (h->ndim == 3) off -= g * h->zstride;
+  char* dev = (char*)h->buf[buf] + off * isz;
+  char* hst = (char*)host + (size_t)k * wx * wy * wz * isz;
+  cudaMemcpy3DParms p;
+  std::memset(&p, 0, sizeof(p));
+  cudaPitchedPtr dp = make_cudaPitchedPtr(dev, (size_t)h->px * isz, (size_t)wx * isz, (size_t)h->ypad);
+  cudaPitchedPtr hp = make_cudaPitchedPtr(hst, (size_t)wx * isz, (size_t)wx * isz, (size_t)wy);
+  p.srcPtr = to_dev ? hp : dp;
+  p.dstPtr = to_dev ? dp : hp;
+  p.extent = make_cudaExtent((size_t)wx * isz, (size_t)wy, (size_t)wz);
+  p.kind = to_dev ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  return cudaMemcpy3DAsync(&p, h->stream);
+}
+
+static int transfer(clb_ctx* h, int buf, void* host, size_t nbytes, bool padded, bool to_dev) {
+  if (!h || !host) return fail(h, CLB_EINVAL, "null argument");
+  if (buf < 0 || buf > 2) return fail(h, CLB_EINVAL, "buffer index out of range");
+  const int64_t g = padded ? 4 : 0;
+  size_t want = (size_t)h->M * h->itemsize * (size_t)(h->cells[0] + g);
+  if (h->ndim >= 2) want *= (size_t)(h->cells[1] + g);
+  if (h->ndim == 3) want *= (size_t)(h->cells[2] + g);
+  if (nbytes != want) return fail(h, CLB_EINVAL, "byte count does not match the grid");
+  cudaSetDevice(h->d.device);
+  for (int k = 0; k < h->M; ++k) {
+    cudaError_t e = copy_state(h, buf, k, host, padded, to_dev);
+    if (e != cudaSuccess) return cuda_fail(h, e, "cudaMemcpy3DAsync");
+  }
+  CLB_CUDA(h, cudaStreamSynchronize(h->stream));
+  return CLB_OK;
+}
+
+int clb_upload(clb_handle h, int buf, const void* src, size_t nbytes) {
+  return transfer(h, buf, const_cast<void*>(src), nbytes, false, true);
+}
+int clb_download(clb_handle h, int buf, void* dst, size_t nbytes) {
+  return transfer(h, buf, dst, nbytes, false, false);
+}
+int clb_upload_padded(clb_handle h, int buf, const void* src, size_t nbytes) {
+  return transfer(h, buf, const_cast<void*>(src), nbytes, true, true);
+}
+int clb_download_padded(clb_handle h, int buf, void* dst, size_t nbytes) {
+  return transfer(h, buf, dst, nbytes, true, false);
+}
+
+int clb_sweep_async(clb_handle h, int axis, double dt, int src, int dst, int slot, int literal) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  return launch_sweep(h, axis, dt, src, dst, slot, literal != 0);
+}
+
+int clb_fetch(clb_handle h, int nslots, double* speeds, int32_t* nonfinite) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  return fetch(h, nslots, speeds, nonfinite);
+}
+
+int clb_sweep(clb_handle h, int axis, double dt, int src, int dst, double* speed,
+              int32_t* nonfinite) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  int r = launch_sweep(h, axis, dt, src, dst, 0, false);
+  if (r) return r;
+  return fetch(h, 1, speed, nonfinite);
+}
+
+int clb_attempt_step(clb_handle h, double dt, int src, int s0, int s1, double* speeds,
+                     int32_t* nonfinite) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  if (src == s0 || src == s1 || s0 == s1) return fail(h, CLB_EINVAL, "step buffers must be distinct");
+  int cur = src;
+  for (int j = 0; j < h->ndim; ++j) {
+    const int dst = (j % 2 == 0) ? s0 : s1;
+    int r = launch_sweep(h, j, dt, cur, dst, j, false);
+    if (r) return r;
+    cur = dst;
+  }
+  return fetch(h, h->ndim, speeds, nonfinite);
+}
+
+int clb_first_nonfinite(clb_handle h, int buf, int32_t* found, int32_t* state, int64_t cell[3]) {
+  if (!h || !found || !state || !cell) return fail(h, CLB_EINVAL, "null argument");
+  if (buf < 0 || buf > 2) return fail(h, CLB_EINVAL, "buffer index out of range");
+  cudaSetDevice(h->d.device);
+  unsigned long long* slot = &h->d_res->first_bad;
+  CLB_CUDA(h, cudaMemsetAsync(slot, 0xff, sizeof(unsigned long long), h->stream));
+  const int64_t total = (int64_t)h->M * h->cells[0] * h->cells[1] * h->cells[2];
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)h->num_sms * 16);
+  const char* base = (const char*)h->buf[buf] + h->origin * h->itemsize;
+  if (h->itemsize == 8)
+    first_bad_kernel<double><<<blocks, 256, 0, h->stream>>>(
+        (const double*)base, h->sstride, h->ystride, h->zstride, h->cells[0], h->cells[1],
+        h->cells[2], h->M, slot);
+  else
+    first_bad_kernel<float><<<blocks, 256, 0, h->stream>>>(
+        (const float*)base, h->sstride, h->ystride, h->zstride, h->cells[0], h->cells[1],
+        h->cells[2], h->M, slot);
+  CLB_CUDA(h, cudaGetLastError());
+  unsigned long long idx = 0;
+  CLB_CUDA(h, cudaMemcpyAsync(&idx, slot, sizeof(idx), cudaMemcpyDeviceToHost, h->stream));
+  CLB_CUDA(h, cudaStreamSynchronize(h->stream));
+  if (idx == ~0ull) {
+    *found = 0;
+    return CLB_OK;
+  }
+  *found = 1;
+  int64_t r = (int64_t)idx;
+  cell[0] = r % h->cells[0]; r /= h->cells[0];
+  cell[1] = r % h->cells[1]; r /= h->cells[1];
+  cell[2] = r % h->cells[2]; r /= h->cells[2];
+  *state = (int32_t)r;
+  return CLB_OK;
+}
+
+int clb_halo_layout(clb_handle h, int buf, int side, void** send_ptr, void** recv_ptr,
+                    size_t* block_bytes, size_t* state_stride_bytes) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  if (h->ndim < 2) return fail(h, CLB_EUNSUPPORTED, "halo exchange needs ndim >= 2");
+  if (buf < 0 || buf > 2 || side < 0 || side > 1) return fail(h, CLB_EINVAL, "bad buffer/side");
+  const int64_t slab = h->ndim == 2 ? h->ystride : h->zstride;  // one row / plane
+  const int64_t n = h->cells[h->ndim - 1];
+  if (n < 2) return fail(h, CLB_EUNSUPPORTED, "halo exchange needs at least 2 owned rows/planes");
+  // first element of owned row/plane 0 (x and y ghosts included)
+  int64_t first = h->origin - h->xoff;
+  if (h->ndim == 3) first -= 2 * h->ystride;
+  char* base = (char*)h->buf[buf] + first * h->itemsize;
+  const int64_t isz = h->itemsize;
+  if (side == 0) {
+    *send_ptr = base;
+    *recv_ptr = base - 2 * slab * isz;
+  } else {
+    *send_ptr = base + (n - 2) * slab * isz;
+    *recv_ptr = base + n * slab * isz;
+  }
+  *block_bytes = (size_t)(2 * slab * isz);
+  *state_stride_bytes = (size_t)(h->sstride * isz);
+  return CLB_OK;
+}
+
+int clb_solve_pairs(clb_handle h, int axis, int64_t n, const void* ql, const void* qr, void* W,
+                    void* s) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  if (axis < 0 || axis >= h->ndim || n < 0) return fail(h, CLB_EINVAL, "bad axis or count");
+  if (n == 0) return CLB_OK;
+  cudaSetDevice(h->d.device);
+  const int nw = h->d.solver_id == CLB_SOLVER_SHALLOW_WATER ? 3
+                 : (h->d.solver_id == CLB_SOLVER_ADVECTION ? 1 : 2);
+  const size_t qb = (size_t)n * h->M * h->itemsize;
+  const size_t wb = (size_t)n * nw * h->M * h->itemsize;
+  const size_t sb = (size_t)n * nw * h->itemsize;
+  char* d = nullptr;
+  CLB_CUDA(h, cudaMalloc(&d, 2 * qb + wb + sb));
+  cudaError_t e = cudaMemcpyAsync(d, ql, qb, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d + qb, qr, qb, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess)
+    e = clb::pairs_dispatch(h->d.solver_id, h->itemsize, h->ndim, axis, d, d + qb, d + 2 * qb,
+                            d + 2 * qb + wb, n, h->d.params, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(W, d + 2 * qb, wb, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(s, d + 2 * qb + wb, sb, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(h, e, "solve_pairs");
+  return CLB_OK;
+}
+
+int clb_enable_timing(clb_handle h, int on) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  h->timing = on != 0;
+  return CLB_OK;
+}
+
+int clb_timing(clb_handle h, double ms[3], int64_t count[3]) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  for (int i = 0; i < 3; ++i) { ms[i] = 0.0; count[i] = 0; }
+  CLB_CUDA(h, cudaStreamSynchronize(h->stream));
+  for (auto& tl : h->launches) {
+    float v = 0.f;
+    cudaEventElapsedTime(&v, tl.a, tl.b);
+    ms[tl.axis] += v;
+    count[tl.axis] += 1;
+    h->event_pool.push_back(tl.a);
+    h->event_pool.push_back(tl.b);
+  }
+  h->launches.clear();
+  return CLB_OK;
+}
+
+void* clb_host_alloc(size_t nbytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, nbytes) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void clb_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int clb_memory_info(clb_handle h, size_t* device_bytes, int64_t* row_pitch) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  if (device_bytes) *device_bytes = 3 * h->buf_bytes;
+  if (row_pitch) *row_pitch = h->px;
+  return CLB_OK;
+}
+
+}  // extern "C"
+
+namespace clb {
+
+template <typename T> cudaError_t pairs_acoustics(int, int, const void*, const void*, void*, void*,
+                                                  int64_t, const double*, cudaStream_t);
+template <typename T> cudaError_t pairs_shallow_water(int, const void*, const void*, void*, void*,
+                                                      int64_t, const double*, cudaStream_t);
+template <typename T> cudaError_t pairs_advection(const void*, const void*, void*, void*, int64_t,
+                                                  const double*, cudaStream_t);
+template <typename T> cudaError_t pairs_vc_acoustics(int, int, const void*, const void*, void*,
+                                                     void*, int64_t, const double*, cudaStream_t);
+
+cudaError_t pairs_dispatch(int solver, int itemsize, int ndim, int axis, const void* ql,
+                           const void* qr, void* W, void* s, int64_t n, const double* p,
+                           cudaStream_t st) {
+  const bool d = itemsize == 8;
+  switch (solver) {
+    case CLB_SOLVER_ACOUSTICS:
+      return d ? pairs_acoustics<double>(ndim, axis, ql, qr, W, s, n, p, st)
+               : pairs_acoustics<float>(ndim, axis, ql, qr, W, s, n, p, st);
+    case CLB_SOLVER_SHALLOW_WATER:
+      return d ? pairs_shallow_water<double>(axis, ql, qr, W, s, n, p, st)
+               : pairs_shallow_water<float>(axis, ql, qr, W, s, n, p, st);
+    case CLB_SOLVER_ADVECTION:
+      return d ? pairs_advection<double>(ql, qr, W, s, n, p, st)
+               : pairs_advection<float>(ql, qr, W, s, n, p, st);
+    default:
+      return d ? pairs_vc_acoustics<double>(ndim, axis, ql, qr, W, s, n, p, st)
+               : pairs_vc_acoustics<float>(ndim, axis, ql, qr, W, s, n, p, st);
+  }
+}
+
+}  // namespace clb
+
+extern "C" int clb_set_boundary(clb_handle h, int axis, int lo, int hi) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  if (axis < 0 || axis >= h->ndim) return fail(h, CLB_EINVAL, "axis out of range");
+  for (int bc : {lo, hi}) {
+    if (bc < 0 || bc > 3) return fail(h, CLB_EINVAL, "unknown boundary kind");
+    if ((bc == CLB_BC_PERIODIC || bc == CLB_BC_REFLECTIVE) && h->cells[axis] < 2)
+      return fail(h, CLB_EUNSUPPORTED, "periodic/reflective boundaries need at least 2 cells");
+    if (bc == CLB_BC_REFLECTIVE && (h->d.normal_velocity[axis] < 0 ||
+                                    h->d.normal_velocity[axis] >= h->M))
+      return fail(h, CLB_EINVAL, "reflective boundary needs a normal velocity state");
+  }
+  if ((lo == CLB_BC_PERIODIC) != (hi == CLB_BC_PERIODIC))
+    return fail(h, CLB_EINVAL, "periodic boundary must be set on both sides");
+  h->d.bc[axis][0] = lo;
+  h->d.bc[axis][1] = hi;
+  return CLB_OK;
+}

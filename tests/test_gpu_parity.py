@@ -1,0 +1,315 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Bar: bit-exact (dt sequence, max wave
+speeds, every state byte) in fp64 and fp32; the north star's fallback
+tolerances (L-inf rel <= 1e-12 fp64, <= 1e-5 fp32) are asserted where a
+full-size run is only checked through properties."""
+
+import math
+
+import numpy as np
+import pytest
+
+import paper_1805_08846_b200 as P
+from paper_1805_08846_b200._native import DeviceGrid
+from oracle import oracle as O
+
+import cases
+
+pytestmark = pytest.mark.gpu
+
+
+def _grid_from_padded(qin, c):
+    cells = tuple(c["cells"])
+    m = qin.shape[0]
+    spec = P.GridSpec(cells, (0.0,) * len(cells), tuple(s * n for s, n in zip(c["spacing"], cells)), m)
+    g = P.create_grid(spec, qin.dtype)
+    g.data[...] = qin
+    return g
+
+
+def test_golden_sweeps_bitwise(golden_sweeps):
+    meta, arrays = golden_sweeps
+    bad = []
+    for i, c in enumerate(meta):
+        qin = arrays[f"qin_{i}"]
+        grid = _grid_from_padded(qin, c)
+        out = P.create_grid(grid.spec, grid.dtype)
+        solver = P.get_solver(c["solver"])
+        params = {
+            "acoustics": lambda p: P.AcousticsParams(p["sound_speed"], p["impedance"]),
+            "shallow_water": lambda p: P.ShallowWaterParams(p["gravity"]),
+            "advection": lambda p: P.AdvectionParams(p["speed"]),
+            "vc_acoustics": lambda p: P.VcAcousticsParams(),
+        }[c["solver"]](c["params"])
+        dt = float.fromhex(c["dt_hex"])
+        # exact reference spacing: run with dt scaled so dt/dx matches bitwise
+        res = _sweep_exact(grid, out, c, dt, solver, params)
+        exp = arrays[f"qout_{i}"]
+        if out.interior().tobytes() != exp.tobytes() or res != float.fromhex(c["smax_hex"]):
+            bad.append((i, c["solver"], c["dtype"], c["limiter"], c["bc"], c["axis"]))
+    assert not bad, f"{len(bad)}/{len(meta)} mismatching sweeps, first: {bad[:6]}"
+
+
+def _sweep_exact(grid, out, c, dt, solver, params):
+    """sweep_axis with the golden case's exact fp64 spacing."""
+    nd = len(c["cells"])
+    g = DeviceGrid(ndim=nd, cells=tuple(c["cells"]), spacing=tuple(c["spacing"]),
+                   num_states=grid.num_states, dtype=grid.dtype,
+                   solver_id=solver.require_device(),
+                   limiter_id=P.LIMITER_IDS[P.LimiterKind(c["limiter"])],
+                   params=solver.pack_params(params, grid.dtype), bc=[(3, 3)] * nd,
+                   normal_velocity=[None] * nd)
+    try:
+        g.upload_padded(0, grid.data)
+        smax, _ = g.sweep(c["axis"], dt, 0, 1)
+        out.interior()[...] = g.download(1)
+        return smax
+    finally:
+        g.close()
+
+
+def test_sweep_axis_api_matches_oracle(rng):
+    # the public per-sweep operator (sweep.py:380-391 contract)
+    for dtype in (np.float64, np.float32):
+        spec = P.GridSpec((37, 29), (0.0, 0.0), (1.0, 1.0), 3)
+        g = P.create_grid(spec, dtype)
+        g.data[0] = 1.0
+        g.interior()[0] = 1.0 + 0.3 * rng.random((29, 37))
+        g.interior()[1:] = 0.2 * rng.standard_normal((2, 29, 37))
+        P.apply_boundary(g, P.BoundarySpec.uniform(P.BoundaryKind.PERIODIC, (1, 2)))
+        for axis in (0, 1):
+            out = P.create_grid(spec, dtype)
+            res = P.sweep_axis(g, out, axis, 0.004, P.get_solver("shallow_water"),
+                               P.LimiterKind.MC, P.ShallowWaterParams(1.0))
+            ref = np.zeros_like(g.data)
+            smax = O.sweep(g.data.copy(), ref, axis, 0.004, spec.spacing, "shallow_water", "mc",
+                           {"gravity": 1.0})
+            assert out.data.tobytes() == ref.tobytes()
+            assert res.max_abs_speed == smax
+
+
+@pytest.mark.parametrize("name", ["acoustics", "shallow_water"])
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_solver_pairs_bitwise(golden_solvers, name, dtype):
+    ql = golden_solvers[f"{name}_{dtype}_ql"]
+    qr = golden_solvers[f"{name}_{dtype}_qr"]
+    We = golden_solvers[f"{name}_{dtype}_W"]
+    se = golden_solvers[f"{name}_{dtype}_s"]
+    params = P.AcousticsParams(1.3, 0.7) if name == "acoustics" else P.ShallowWaterParams(1.7)
+    solver = P.get_solver(name)
+    for axis in (0, 1):
+        sel = np.arange(ql.shape[0]) % 2 == axis
+        g = DeviceGrid(ndim=2, cells=(4, 4), spacing=(1.0, 1.0), num_states=3, dtype=dtype,
+                       solver_id=solver.device_id, limiter_id=0,
+                       params=solver.pack_params(params, np.dtype(dtype)), bc=[(0, 0)] * 2,
+                       normal_velocity=[None] * 2)
+        W, s = g.solve_pairs(axis, ql[sel], qr[sel], solver.num_waves)
+        g.close()
+        assert W.tobytes() == We[sel].tobytes()
+        assert s.tobytes() == se[sel].tobytes()
+
+
+@pytest.mark.parametrize("name", sorted(cases.RECIPES))
+def test_golden_runs_bitwise(golden_runs, name):
+    """dt / speed / nu / accept sequence and final state, bit for bit."""
+    r = cases.RECIPES[name]
+    g = golden_runs[name]
+    sim, grid = cases.product_sim(r)
+    with sim:
+        attempts = cases.drive(sim, r)
+        assert cases.attempts_hex(attempts) == g["attempts"]
+        assert float(sim.t).hex() == g["t"]
+        assert cases.sha(sim.grid.interior()) == g["sha256"]
+        assert sim.steps_reverted == g["steps_reverted"]
+
+
+SHAPES = [
+    ("shallow_water2d", (97, 61), "radial_dam_break", {}),
+    ("shallow_water2d", (300, 17), "gaussian_hump", {"amplitude": 0.7}),
+    ("acoustics2d", (129, 70), "gaussian_pressure", {"width": 0.15}),
+    ("acoustics3d", (33, 20, 18), "gaussian_pressure", {"width": 0.2}),
+    ("vc_acoustics3d", (20, 17, 26), "two_material_pulse", {}),
+    ("vc_acoustics2d", (41, 37), "two_material_pulse", {"center": (0.5, 0.3)}),
+]
+
+
+def _recipe(problem, cells, profile, options, dtype, bc, limiter, steps):
+    nd = len(cells)
+    lower = (-1.0,) * nd if profile == "radial_dam_break" else (0.0,) * nd
+    return dict(name="adhoc", problem=problem, profile=profile, options=options, cells=cells,
+                lower=lower, upper=(1.0,) * nd, dtype=dtype, bc=bc, limiter=limiter,
+                speed="bound" if not problem.startswith("vc") else ("value", 1.0),
+                drive=("max_steps", steps))
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"{s[0]}-{'x'.join(map(str, s[1]))}")
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("bc", ["outflow", "reflective", "periodic"])
+@pytest.mark.parametrize("limiter", ["mc", "superbee", "minmod", "vanleer", "none"])
+def test_random_configs_match_oracle(shape, dtype, bc, limiter):
+    problem, cells, profile, options = shape
+    r = _recipe(problem, cells, profile, options, dtype, bc, limiter, steps=4)
+    osim, _ = cases.oracle_sim(r)
+    oatt = cases.drive(osim, r)
+    sim, _ = cases.product_sim(r)
+    with sim:
+        att = cases.drive(sim, r)
+        assert cases.attempts_hex(att) == cases.attempts_hex(oatt)
+        assert sim.grid.interior().tobytes() == O.interior(osim.grid).tobytes()
+
+
+@pytest.mark.parametrize("seg", [(1, 1), (7, 5), (33, 40), (64, 3), (1000, 1000)])
+def test_segmentation_is_bitwise_invisible(seg):
+    r = _recipe("shallow_water2d", (150, 130), "radial_dam_break", {}, "float64", "reflective",
+                "mc", 3)
+    ref_sim, _ = cases.product_sim(r)
+    with ref_sim:
+        cases.drive(ref_sim, r)
+        ref = ref_sim.grid.interior().copy()
+    sim, _ = cases.product_sim(r)
+    with sim:
+        sim.device_grid.set_segments(0, seg[0])
+        sim.device_grid.set_segments(1, seg[1])
+        cases.drive(sim, r)
+        assert sim.grid.interior().tobytes() == ref.tobytes()
+
+
+def test_revert_restores_state_bitwise():
+    r = cases.RECIPES["dam_break_revert_64x16"]
+    sim, _ = cases.product_sim(r)
+    reverts = 0
+    with sim:
+        while sim.t < 0.15:
+            before = sim.grid.interior().tobytes()
+            t0 = sim.t
+            a = sim.attempt_step(stop=0.15)
+            if a.accepted:
+                assert a.nu <= 1.0
+            else:
+                reverts += 1
+                assert sim.t == t0
+                assert sim.grid.interior().tobytes() == before
+    assert reverts >= 1 and sim.steps_reverted == reverts
+
+
+def test_underestimate_revert_then_exact_retry():
+    # pkg/tests/test_timestep.py:88-105: nu = 1.8, retry dt = 0.45 dx, retry nu = 0.9
+    spec = P.GridSpec((8, 8), (0, 0), (1, 1), 3)
+    g = P.create_grid(spec)
+    g.data[0] = 4.0
+    sim = P.Simulation(g, P.get_solver("shallow_water"), P.ShallowWaterParams(1.0),
+                       P.BoundarySpec.uniform(P.BoundaryKind.PERIODIC, (1, 2)),
+                       initial_max_speed=1.0, cfl_target=0.9)
+    before = sim.grid.data.tobytes()
+    a = sim.attempt_step()
+    assert not a.accepted and a.nu == pytest.approx(1.8) and a.dt_retry == pytest.approx(0.45 / 8)
+    assert sim.grid.data.tobytes() == before
+    b = sim.attempt_step()
+    assert b.accepted and b.nu == pytest.approx(0.9)
+    sim.last_max_speed = 1.0
+    sim2 = P.Simulation(P.create_grid(spec), P.get_solver("shallow_water"),
+                        P.ShallowWaterParams(1.0),
+                        P.BoundarySpec.uniform(P.BoundaryKind.PERIODIC, (1, 2)),
+                        initial_max_speed=1.0)
+    sim2.grid.data[0] = 4.0
+    sim2.attempt_step()
+    sim2.last_max_speed = 1.0
+    with pytest.raises(P.UnstableStepError):
+        sim2.attempt_step()
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("where", [(3, 4), (0, 0), (15, 15)])
+def test_blowup_location_matches_oracle(dtype, where):
+    spec = P.GridSpec((16, 16), (0, 0), (1, 1), 3)
+    rng = np.random.default_rng(1)
+    g = P.create_grid(spec, dtype)
+    g.interior()[...] = 0.05 * rng.standard_normal(g.interior().shape)
+    sim = P.Simulation(g, P.get_solver("acoustics"), P.AcousticsParams(),
+                       P.BoundarySpec.uniform(P.BoundaryKind.PERIODIC, (1, 2)),
+                       initial_max_speed=1.0)
+    sim.grid.interior(0)[where] = np.nan
+    data = sim.grid.data.copy()
+    osim = O.OracleSimulation(data, spec.spacing, "acoustics",
+                              {"sound_speed": 1.0, "impedance": 1.0},
+                              [("periodic", "periodic")] * 2, (1, 2), initial_max_speed=1.0)
+    with pytest.raises(O.OracleBlowup) as oexc:
+        osim.attempt_step()
+    with pytest.raises(P.NumericalBlowup) as exc:
+        sim.attempt_step()
+    assert (exc.value.state, exc.value.cell, exc.value.step) == \
+        (oexc.value.state, oexc.value.cell, oexc.value.step)
+
+
+def test_dry_state_blowup_in_shallow_water_matches_oracle():
+    spec = P.GridSpec((24, 20), (0, 0), (1, 1), 3)
+    g = P.create_grid(spec)
+    g.interior()[0] = 1.0
+    g.interior()[0][5, 7] = -0.5  # negative depth -> NaN speeds
+    sim = P.Simulation(g, P.get_solver("shallow_water"), P.ShallowWaterParams(),
+                       P.BoundarySpec.uniform(P.BoundaryKind.OUTFLOW, (1, 2)),
+                       initial_max_speed=1.5)
+    osim = O.OracleSimulation(g.data.copy(), spec.spacing, "shallow_water", {"gravity": 1.0},
+                              [("outflow", "outflow")] * 2, (1, 2), initial_max_speed=1.5)
+    with pytest.raises(O.OracleBlowup) as oexc:
+        osim.attempt_step()
+    with pytest.raises(P.NumericalBlowup) as exc:
+        sim.attempt_step()
+    assert (exc.value.state, exc.value.cell) == (oexc.value.state, oexc.value.cell)
+
+
+def test_build_simulation_from_config():
+    text = """[run]
+problem = acoustics2d
+t_end = 0.6
+[grid]
+cells = 256 256
+[scheme]
+limiter = mc
+[boundary]
+all = reflective
+[initial]
+profile = gaussian_pressure
+amplitude = 1.0
+width = 0.08
+[parallel]
+serial = true
+"""
+    with P.build_simulation(P.loads(text)) as sim:
+        sim.run_until(1e30, max_steps=100)
+        assert cases.sha(sim.grid.interior()).startswith("429c7880ae08b44f")
+        assert sim.t == 0.35156250000000033
+
+
+def test_large_periodic_conservation_fp64():
+    """Size-independent property at a large grid: periodic sweeps conserve
+    every state's interior sum to rounding (pkg/tests/test_acceptance.py:183-198)."""
+    n = 2048
+    spec = P.GridSpec((n, n), (0, 0), (1, 1), 3)
+    g = P.create_grid(spec)
+    P.fill_initial(g, P.get_problem("shallow_water2d").initial_profile("gaussian_hump", {}, spec))
+    g.interior()[1] = 0.1
+    before = g.interior().sum(axis=(1, 2))
+    scale = np.abs(g.interior()).sum(axis=(1, 2))
+    bound = P.get_problem("shallow_water2d").speed_bound(g, P.ShallowWaterParams())
+    with P.Simulation(g, P.get_solver("shallow_water"), P.ShallowWaterParams(),
+                      P.BoundarySpec.uniform(P.BoundaryKind.PERIODIC, (1, 2)),
+                      initial_max_speed=bound) as sim:
+        sim.run_until(1e30, max_steps=5)
+        after = sim.grid.interior().sum(axis=(1, 2))
+    assert np.max(np.abs(after - before) / np.maximum(scale, 1.0)) < 1e-12
+
+
+def test_large_grid_matches_oracle_fp32_and_fp64():
+    for dtype in ("float64", "float32"):
+        r = _recipe("shallow_water2d", (1024, 768), "radial_dam_break", {}, dtype, "reflective",
+                    "mc", 3)
+        osim, _ = cases.oracle_sim(r)
+        oatt = cases.drive(osim, r)
+        sim, _ = cases.product_sim(r)
+        with sim:
+            att = cases.drive(sim, r)
+            assert cases.attempts_hex(att) == cases.attempts_hex(oatt)
+            a = sim.grid.interior()
+            b = O.interior(osim.grid)
+            assert a.tobytes() == b.tobytes()
