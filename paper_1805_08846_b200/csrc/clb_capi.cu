@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -112,7 +113,26 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   g.lim_id = h->d.limiter_id;
   g.num_sms = h->num_sms;
   const int64_t nx = h->cells[0], ny = h->cells[1], nz = h->cells[2];
-  if (axis == 0) {
+  static const int xmode = [] {
+    const char* e = getenv("CLB_XSWEEP");
+    return (e && e[0] == 'B') ? 2 : 1;
+  }();
+  if (axis == 0 && xmode == 2) {
+    // experiment: thread-per-row marching along x (lanes across rows)
+    g.contig = 2;
+    g.n = (int)nx; g.n1 = (int)ny; g.n2 = (int)nz;
+    g.astride = 1; g.t1stride = h->ystride; g.t2stride = h->zstride;
+    const int64_t cols = ny * nz;
+    const int64_t target_threads = (int64_t)h->num_sms * 2048;
+    int64_t nseg = (target_threads + cols - 1) / cols;
+    nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, nx / 32));
+    int64_t L = (nx + nseg - 1) / nseg;
+    if (h->seg_override[0] > 0) L = h->seg_override[0];
+    g.seg_len = (int)L;
+    g.nseg = (int)((nx + L - 1) / L);
+    g.block = 128;
+    if (nz > 1) { g.n1 = (int)(ny); }
+  } else if (axis == 0) {
     g.contig = 1;
     g.n = (int)nx; g.n1 = (int)ny; g.n2 = (int)nz;
     g.astride = 1; g.t1stride = h->ystride; g.t2stride = h->zstride;

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(128) sweep_strided(const SweepArgs<T> a) {
   T smax = T(0);
   uint32_t fin = 0xffffffffu;
   if (x < a.n1) {
-    const int64_t off = (int64_t)x + (int64_t)t2 * a.t2stride;
+    const int64_t off = (int64_t)x * a.t1stride + (int64_t)t2 * a.t2stride;
     const T* qc = a.qin + off;
     T* oc = a.qout + off;
     const int lo = seg * a.seg_len;
@@ -351,7 +351,7 @@ inline SweepArgs<T> to_args(const GenericArgs& g) {
 template <typename T, class S, bool LIT>
 inline cudaError_t launch_one(const GenericArgs& g, cudaStream_t st) {
   SweepArgs<T> a = to_args<T>(g);
-  if (g.contig) {
+  if (g.contig == 1) {
     const int64_t warps = (int64_t)g.n1 * g.n2 * g.nseg;
     const int64_t blocks = (warps + 3) / 4;
     sweep_contig<T, S, LIT><<<(unsigned)blocks, 128, 0, st>>>(a);
