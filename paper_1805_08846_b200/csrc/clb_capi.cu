@@ -113,38 +113,21 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   g.lim_id = h->d.limiter_id;
   g.num_sms = h->num_sms;
   const int64_t nx = h->cells[0], ny = h->cells[1], nz = h->cells[2];
-  static const int xmode = [] {
-    const char* e = getenv("CLB_XSWEEP");
-    return (e && e[0] == 'B') ? 2 : 1;
+  // Work decomposition: 128 pencils per CTA; segments along the sweep axis
+  // until ~6 CTAs per SM are in flight, but never shorter than 32 cells (each
+  // segment re-reads 4 cells and re-solves 3 fans of its neighbour).
+  const int64_t target_ctas = (int64_t)h->num_sms * 6;
+  int64_t pen_ctas;
+  static const int contig_mode = [] {
+    const char* e = getenv("CLB_CONTIG");
+    return (e && e[0] == 't') ? 2 : 1;
   }();
-  if (axis == 0 && xmode == 2) {
-    // experiment: thread-per-row marching along x (lanes across rows)
-    g.contig = 2;
+  if (axis == 0) {
+    g.contig = contig_mode;
     g.n = (int)nx; g.n1 = (int)ny; g.n2 = (int)nz;
     g.astride = 1; g.t1stride = h->ystride; g.t2stride = h->zstride;
-    const int64_t cols = ny * nz;
-    const int64_t target_threads = (int64_t)h->num_sms * 2048;
-    int64_t nseg = (target_threads + cols - 1) / cols;
-    nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, nx / 32));
-    int64_t L = (nx + nseg - 1) / nseg;
-    if (h->seg_override[0] > 0) L = h->seg_override[0];
-    g.seg_len = (int)L;
-    g.nseg = (int)((nx + L - 1) / L);
-    g.block = 128;
-    if (nz > 1) { g.n1 = (int)(ny); }
-  } else if (axis == 0) {
-    g.contig = 1;
-    g.n = (int)nx; g.n1 = (int)ny; g.n2 = (int)nz;
-    g.astride = 1; g.t1stride = h->ystride; g.t2stride = h->zstride;
-    const int64_t rows = ny * nz;
-    const int64_t target_warps = (int64_t)h->num_sms * 32;
-    int64_t nseg = (target_warps + rows - 1) / rows;
-    nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, nx / 64));
-    int64_t L = (nx + nseg - 1) / nseg;
-    if (h->seg_override[0] > 0) L = h->seg_override[0];
-    g.seg_len = (int)L;
-    g.nseg = (int)((nx + L - 1) / L);
-    g.block = 128;
+    // warp-marching: one warp per (row, segment), 4 warps per CTA
+    pen_ctas = contig_mode == 1 ? (ny * nz + 3) / 4 : (ny * nz + 127) / 128;
   } else {
     g.contig = 0;
     g.n1 = (int)nx;
@@ -154,16 +137,17 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
     } else {
       g.n = (int)nz; g.n2 = (int)ny; g.astride = h->zstride; g.t2stride = h->ystride;
     }
-    const int64_t cols = nx * (int64_t)g.n2;
-    const int64_t target_threads = (int64_t)h->num_sms * 2048;
-    int64_t nseg = (target_threads + cols - 1) / cols;
-    nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, g.n / 32));
-    int64_t L = (g.n + nseg - 1) / nseg;
-    if (h->seg_override[axis] > 0) L = h->seg_override[axis];
-    g.seg_len = (int)L;
-    g.nseg = (int)((g.n + L - 1) / L);
-    g.block = nx >= 128 ? 128 : (nx >= 64 ? 64 : 32);
+    pen_ctas = ((nx + 127) / 128) * g.n2;
   }
+  // contig stages are 48 bytes of a row: segment starts must stay aligned
+  const int64_t align = (axis == 0 && contig_mode == 2) ? 48 / h->itemsize : 1;
+  int64_t nseg = (target_ctas + pen_ctas - 1) / pen_ctas;
+  nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, g.n / 32));
+  int64_t L = (g.n + nseg - 1) / nseg;
+  if (h->seg_override[axis] > 0) L = h->seg_override[axis];
+  L = (L + align - 1) / align * align;
+  g.seg_len = (int)L;
+  g.nseg = (int)((g.n + L - 1) / L);
   return g;
 }
 
@@ -283,7 +267,8 @@ int clb_create(const clb_desc* desc, clb_handle* out) {
   for (int ax = 0; ax < d.ndim; ++ax) h->cells[ax] = d.cells[ax];
   const int64_t align = 128 / d.itemsize;
   h->xoff = align;
-  h->px = (h->xoff + h->cells[0] + 2 + align - 1) / align * align;
+  // slack past the x ghosts: contig stages may read up to 13 cells beyond n+1
+  h->px = (h->xoff + h->cells[0] + 16 + align - 1) / align * align;
   h->ypad = d.ndim >= 2 ? h->cells[1] + 4 : 1;
   h->zpad = d.ndim == 3 ? h->cells[2] + 4 : 1;
   h->ystride = h->px;

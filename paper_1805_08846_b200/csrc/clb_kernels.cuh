@@ -1,31 +1,35 @@
-// clb_kernels.cuh -- the fused directional sweep kernels for sm_100a.
+// clb_kernels.cuh -- the fused directional sweep kernel for sm_100a.
 //
-// One kernel launch == one directional sweep of the reference
-// (sweep.py:307-377 sweep_axis_tiled over sweep.py:183-263 sweep_tile),
-// with the ghost-cell fill of boundary.py:87-122 fused in as an index remap
-// at load time, the per-sweep max |s| folded by warp shuffle + block
-// reduction + one guarded atomicMax, and the non-finite check of
-// timestep.py:179-186 folded into the store epilogue on the integer pipe.
+// One launch == one directional sweep of the reference (sweep.py:307-377
+// sweep_axis_tiled over sweep.py:183-263 sweep_tile) with
+//   * the ghost-cell fill of boundary.py:87-122 fused in as a read-side index
+//     remap (physical boundaries) or a plain read of memory ghosts (HALO),
+//   * the per-sweep max |s| folded by warp shuffle + block reduction + one
+//     guarded atomicMax,
+//   * the non-finite check of timestep.py:179-186 folded into the store
+//     epilogue on the integer pipe.
 //
-// Two thread mappings, both reading and writing each cell once per segment
-// with fully coalesced 128-byte transactions:
+// Thread mapping: one thread per pencil, marching along the sweep axis with
+// the reference's three-fan ring (sweep.py:195-200) held in registers.  The
+// ring is unrolled by its period (3) so slot rotation costs no moves.
 //
-//  * sweep_contig (axis 0, x, unit stride): a warp marches along one row
-//    in 32-cell chunks, lane l owning cell b+l.  Interface fans, correction
-//    fluxes and cell updates trail each other by one and two lanes, handed
-//    over with __shfl_sync; the two lanes that cross a chunk boundary take
-//    their neighbours from a per-warp shared-memory carry slot.
-//
-//  * sweep_strided (axes 1, 2): one thread per x column marches along the
-//    sweep axis with a three-fan register ring (the reference's ring,
-//    sweep.py:195-200) and a one-cell register prefetch; a warp covers 32
-//    consecutive x, so every load/store is one coalesced row segment.
-//
-// Rows/columns are split into segments along the sweep axis; each segment
-// recomputes the 3 fans it shares with its neighbour exactly as the
-// reference's tiles do (sweep.py:11-16), so results are bitwise independent
-// of the segmentation.
+// Data movement: a CTA = 4 consumer warps (128 pencils) + 1 producer warp.
+// The producer streams the pencils' cells, NC per pencil per stage, into a
+// shared-memory ring with cp.async.bulk (TMA engine) tracked by mbarriers
+// (full/empty per stage), so HBM latency hides behind NSTAGE-1 stages of
+// prefetch while consumers compute:
+//   * strided sweeps (y, z): a stage is NC rows of 128 consecutive x-cells
+//     per state -- one contiguous bulk copy per row and state; consumer t
+//     reads column t (bank-conflict free);
+//   * the contiguous sweep (x): a stage is 48 bytes (NC cells) of each of
+//     128 rows per state -- one bulk copy per row and state, issued by all
+//     32 producer lanes; consumer t reads its own row (a transpose through
+//     shared memory, so the x-sweep needs no warp shuffles).
+// Segments along the sweep axis recompute the fans they share with their
+// neighbour exactly as the reference's tiles do (sweep.py:11-16), so results
+// are bitwise independent of the segmentation.
 #pragma once
+#include "clb_async.cuh"
 #include "clb_solvers.cuh"
 
 namespace clb {
@@ -33,13 +37,16 @@ namespace clb {
 enum { BC_OUTFLOW = 0, BC_REFLECTIVE = 1, BC_PERIODIC = 2, BC_HALO = 3 };
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int kConsumers = 128;        // pencils per CTA
+constexpr int kThreads = kConsumers + 32;
+constexpr int kRowStrideContig = 48;   // bytes per row per state in a contig stage
 
 template <typename T> struct SweepArgs {
   const T* qin;     // element (0,0,0) of state 0 (interior origin)
   T* qout;
   int64_t sstride;  // elements between states
   int64_t astride;  // element stride along the sweep axis
-  int64_t t1stride; // contig: row stride of transverse axis 1 (y); strided: 1 (x)
+  int64_t t1stride; // stride of transverse axis 1 (strided: x = 1; contig: y rows)
   int64_t t2stride; // remaining transverse axis
   int n;            // cells along the sweep axis
   int n1, n2;       // transverse extents
@@ -60,7 +67,7 @@ __device__ __forceinline__ int remap(int j, int n, int lo, int hi, bool& neg) {
     if (lo == BC_OUTFLOW) return 0;
     if (lo == BC_PERIODIC) return n + j;
     if (lo == BC_REFLECTIVE) { neg = true; return -1 - j; }
-    return j;  // halo rows live in memory
+    return j;  // halo / caller-filled ghosts live in memory
   }
   if (j >= n) {
     if (hi == BC_OUTFLOW) return n - 1;
@@ -69,23 +76,6 @@ __device__ __forceinline__ int remap(int j, int n, int lo, int hi, bool& neg) {
     return j;
   }
   return j;
-}
-
-template <typename T> __device__ __forceinline__ T ld_nc(const T* p) { return __ldg(p); }
-
-template <typename T, int M>
-__device__ __forceinline__ void load_cell(const T* base, int64_t sstride, int64_t astride, int j,
-                                          const SweepArgs<T>& a, T (&q)[M]) {
-  bool neg;
-  const int js = remap(j, a.n, a.bc_lo, a.bc_hi, neg);
-  const T* p = base + (int64_t)js * astride;
-#pragma unroll
-  for (int k = 0; k < M; ++k) q[k] = ld_nc(p + k * sstride);
-  if (neg) {
-#pragma unroll
-    for (int k = 0; k < M; ++k)
-      if (k == a.nv) q[k] = -q[k];
-  }
 }
 
 // Warp + block reduction of (max |s|, finite key), one guarded atomic per block.
@@ -115,6 +105,289 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
   }
 }
 
+// Resident CTAs per SM the register allocation is sized for: the fp64
+// shallow-water march needs ~150 registers (2 CTAs), everything else fits 3.
+template <typename T, class S> constexpr int kMinBlocks() {
+  return (sizeof(T) == 8 && S::NW >= 3) ? 2 : 3;
+}
+
+template <typename T, class S, bool CONTIG> struct StageGeom {
+  static constexpr int NC = CONTIG ? (kRowStrideContig / (int)sizeof(T)) : 3;  // cells/stage
+  static constexpr int BYTES = CONTIG ? S::M * kConsumers * kRowStrideContig
+                                      : S::M * NC * kConsumers * (int)sizeof(T);
+  static constexpr int NSTAGE = (72 * 1024 / BYTES) < 2 ? 2
+                                : ((72 * 1024 / BYTES) > 6 ? 6 : (72 * 1024 / BYTES));
+  static constexpr int SMEM = NSTAGE * BYTES + 2 * NSTAGE * 8;
+};
+
+// ---------------------------------------------------------------------------
+// The ring-march state of one pencil.  Slot p holds interface/cell index
+// i with i % 3 == p; P is the slot of the incoming cell.
+template <typename T, class S, int LIM, bool LIT> struct March {
+  using Cell = typename S::Cell;
+  using Fan = typename S::Fan;
+  static constexpr int M = S::M;
+  Cell X[3];
+  Fan F[3];
+  T G[3][M];
+  T smax;
+  uint32_t fin;
+
+  __device__ __forceinline__ int lim(const SweepArgs<T>& a) const { return LIM >= 0 ? LIM : a.lim_id; }
+
+  // prologue steps (no output)
+  template <int P> __device__ __forceinline__ void first(const T (&q)[M]) { X[P] = S::make(q); }
+  template <int P> __device__ __forceinline__ void fan(const T (&q)[M], const SweepArgs<T>& a,
+                                                       bool fold) {
+    constexpr int P1 = (P + 2) % 3;
+    X[P] = S::make(q);
+    F[P] = S::solve(X[P1], X[P], a.P);
+    if (fold) fold_speed<S, T>(F[P], a.P, smax);
+  }
+  template <int P> __device__ __forceinline__ void fan_corr(const T (&q)[M],
+                                                            const SweepArgs<T>& a, bool fold) {
+    constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
+    fan<P>(q, a, fold);
+    correction<S, LIT, T>(F[P2], F[P1], F[P], a.P, a.dtdx, lim(a), G[P1]);
+  }
+  // steady step: returns the updated cell i-2 in `out`
+  template <int P> __device__ __forceinline__ void step(const T (&q)[M], const SweepArgs<T>& a,
+                                                        bool fold, T (&out)[M]) {
+    constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
+    fan_corr<P>(q, a, fold);
+    update<S, LIT, T>(X[P2].q, F[P2], F[P1], G[P1], G[P2], a.P, a.dtdx, out);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// The sweep kernel.  Relative cell index r = 0 .. L+5 of a segment [lo, hi)
+// maps to pencil cell j = lo - 4 + r: r = 0, 1 are alignment dummies, r = 2..5
+// the prologue (cells lo-2 .. lo+1), r >= 6 emits cell lo + r - 6.
+template <typename T, class S, int LIM, bool LIT, bool CONTIG>
+__global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>()) sweep_kernel(const SweepArgs<T> a) {
+  using G = StageGeom<T, S, CONTIG>;
+  constexpr int NC = G::NC, NSTAGE = G::NSTAGE, M = S::M;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * G::BYTES);
+  uint64_t* empty = full + NSTAGE;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int seg = blockIdx.y;
+  const int lo = seg * a.seg_len;
+  const int hi = min(a.n, lo + a.seg_len);
+  const int ncell = hi - lo + 6;
+  const int nst = (ncell + NC - 1) / NC;
+  // pencil block
+  const int64_t pb = (int64_t)blockIdx.x * kConsumers;
+  const int64_t npen = CONTIG ? (int64_t)a.n1 * a.n2 : (int64_t)a.n1;
+  const int nvalid = (int)(npen - pb < (int64_t)kConsumers ? npen - pb : (int64_t)kConsumers);
+
+  if (tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  T smax = T(0);
+  uint32_t fin = 0xffffffffu;
+
+  if (warp == kConsumers / 32) {
+    // ------------------------------ producer ------------------------------
+    constexpr int isz = (int)sizeof(T);
+    if (!CONTIG) {
+      const int64_t x0 = pb;
+      const uint32_t colbytes = (uint32_t)(((nvalid * isz) + 15) & ~15);
+      const T* base = a.qin + x0 + (int64_t)blockIdx.z * a.t2stride;
+      if (lane == 0) {
+        for (int k = 0; k < nst; ++k) {
+          const int s = k % NSTAGE;
+          if (k >= NSTAGE) mbar_wait(&empty[s], ((k / NSTAGE) - 1) & 1);
+          int r0 = k * NC, r1 = min(ncell, r0 + NC);
+          const int rs = max(r0, 2);
+          const uint32_t bytes = (r1 > rs ? (uint32_t)(r1 - rs) : 0u) * M * colbytes;
+          mbar_arrive_expect_tx(&full[s], bytes);
+          unsigned char* st = smem + s * G::BYTES;
+          for (int r = rs; r < r1; ++r) {
+            bool neg;
+            const int js = remap(lo - 4 + r, a.n, a.bc_lo, a.bc_hi, neg);
+            const T* src = base + (int64_t)js * a.astride;
+#pragma unroll
+            for (int q = 0; q < M; ++q)
+              bulk_g2s(st + ((q * NC + (r - r0)) * kConsumers) * isz, src + q * a.sstride,
+                       colbytes, &full[s]);
+          }
+        }
+      }
+    } else {
+      // rows owned by this lane: lane, lane+32, lane+64, lane+96
+      const T* rowp[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t R = pb + lane + 32 * u;
+        const int y = (int)(R % a.n1), z = (int)(R / a.n1);
+        rowp[u] = a.qin + (int64_t)y * a.t1stride + (int64_t)z * a.t2stride;
+      }
+      for (int k = 0; k < nst; ++k) {
+        const int s = k % NSTAGE;
+        if (k >= NSTAGE) mbar_wait(&empty[s], ((k / NSTAGE) - 1) & 1);
+        if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(nvalid * M * kRowStrideContig));
+        __syncwarp();
+        unsigned char* st = smem + s * G::BYTES;
+        const int x = lo - 4 + k * NC;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = lane + 32 * u;
+          if (t < nvalid) {
+#pragma unroll
+            for (int q = 0; q < M; ++q)
+              bulk_g2s(st + (q * kConsumers + t) * kRowStrideContig, rowp[u] + q * a.sstride + x,
+                       kRowStrideContig, &full[s]);
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------ consumers ------------------------------
+    const int t = tid;
+    const bool active = t < nvalid;
+    March<T, S, LIM, LIT> mr;
+    mr.smax = T(0);
+    mr.fin = 0xffffffffu;
+    // pencil addressing for stores / ghost loads
+    const T* pin;
+    T* pout;
+    int64_t step_el;
+    if (CONTIG) {
+      const int64_t R = pb + (active ? t : 0);
+      const int y = (int)(R % a.n1), z = (int)(R / a.n1);
+      const int64_t off = (int64_t)y * a.t1stride + (int64_t)z * a.t2stride;
+      pin = a.qin + off;
+      pout = a.qout + off;
+      step_el = 1;
+    } else {
+      const int64_t off = pb + (active ? t : 0) + (int64_t)blockIdx.z * a.t2stride;
+      pin = a.qin + off;
+      pout = a.qout + off;
+      step_el = a.astride;
+    }
+    const bool halo_lo = a.bc_lo == BC_HALO, halo_hi = a.bc_hi == BC_HALO;
+    const bool refl_lo = a.bc_lo == BC_REFLECTIVE, refl_hi = a.bc_hi == BC_REFLECTIVE;
+
+    auto fetch = [&](const unsigned char* st, int r, int c, T (&q)[M]) {
+      const int j = lo - 4 + r;
+      if (!CONTIG) {
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          q[k] = reinterpret_cast<const T*>(st)[(k * NC + c) * kConsumers + t];
+        const bool neg = (j < 0 && refl_lo) || (j >= a.n && refl_hi);
+        if (neg) {
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+            if (k == a.nv) q[k] = -q[k];
+        }
+      } else {
+        const bool ghost = (j < 0 && !halo_lo) || (j >= a.n && !halo_hi);
+        if (!ghost) {
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+            q[k] = *reinterpret_cast<const T*>(st + (k * kConsumers + t) * kRowStrideContig +
+                                               c * (int)sizeof(T));
+        } else {
+          bool neg;
+          const int js = remap(j, a.n, a.bc_lo, a.bc_hi, neg);
+#pragma unroll
+          for (int k = 0; k < M; ++k) q[k] = pin[js + k * a.sstride];
+          if (neg) {
+#pragma unroll
+            for (int k = 0; k < M; ++k)
+              if (k == a.nv) q[k] = -q[k];
+          }
+        }
+      }
+    };
+    auto emit = [&](int r, const T (&o)[M]) {
+      T* dst = pout + (int64_t)(lo + r - 6) * step_el;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        dst[k * a.sstride] = o[k];
+        mr.fin = min(mr.fin, finite_key(o[k]));
+      }
+    };
+
+    for (int k = 0; k < nst; ++k) {
+      const int s = k % NSTAGE;
+      mbar_wait(&full[s], (k / NSTAGE) & 1);
+      const unsigned char* st = smem + s * G::BYTES;
+#pragma unroll 1
+      for (int g = 0; g < NC / 3; ++g) {
+        const int r0 = k * NC + 3 * g;
+        if (r0 >= ncell) break;
+        const int c0 = 3 * g;
+        T q[M];
+        if (r0 >= 6) {
+          T o[M];
+          bool v;
+          fetch(st, r0, c0, q);
+          v = r0 < ncell;
+          mr.template step<0>(q, a, v && active, o);
+          if (v && active) emit(r0, o);
+          fetch(st, r0 + 1, c0 + 1, q);
+          v = r0 + 1 < ncell;
+          mr.template step<1>(q, a, v && active, o);
+          if (v && active) emit(r0 + 1, o);
+          fetch(st, r0 + 2, c0 + 2, q);
+          v = r0 + 2 < ncell;
+          mr.template step<2>(q, a, v && active, o);
+          if (v && active) emit(r0 + 2, o);
+        } else if (r0 == 3) {
+          fetch(st, 3, c0, q);
+          mr.template fan<0>(q, a, active);          // F(lo-1)
+          fetch(st, 4, c0 + 1, q);
+          mr.template fan<1>(q, a, active);          // F(lo)
+          fetch(st, 5, c0 + 2, q);
+          mr.template fan_corr<2>(q, a, active);     // F(lo+1), G(lo)
+        } else {
+          fetch(st, 2, c0 + 2, q);
+          mr.template first<2>(q);                   // cell lo-2
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    smax = mr.smax;
+    fin = mr.fin;
+  }
+  finish_block<T>(smax, fin, a);
+}
+
+// ---------------------------------------------------------------------------
+// Axis 0 (x, unit stride) -- warp-marching variant.  A warp marches along one
+// row in 32-cell chunks, lane l owning cell b+l; interface fans, correction
+// fluxes and cell updates trail each other by one and two lanes and are
+// handed over with __shfl_sync (the two lanes that cross a chunk boundary
+// take their neighbours from a per-warp shared-memory carry slot).  Loads
+// and stores are fully coalesced.
+template <typename T> __device__ __forceinline__ T ld_nc(const T* p) { return __ldg(p); }
+
+template <typename T, int M>
+__device__ __forceinline__ void load_cell(const T* base, int64_t sstride, int64_t astride, int j,
+                                          const SweepArgs<T>& a, T (&q)[M]) {
+  bool neg;
+  const int js = remap(j, a.n, a.bc_lo, a.bc_hi, neg);
+  const T* p = base + (int64_t)js * astride;
+#pragma unroll
+  for (int k = 0; k < M; ++k) q[k] = ld_nc(p + k * sstride);
+  if (neg) {
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+      if (k == a.nv) q[k] = -q[k];
+  }
+}
+
 template <typename T, class S> struct CarryLayout {
   static constexpr int kCell = (int)(sizeof(typename S::Cell) / sizeof(T));
   static constexpr int kFan = (int)(sizeof(typename S::Fan) / sizeof(T));
@@ -123,8 +396,9 @@ template <typename T, class S> struct CarryLayout {
 
 // ---------------------------------------------------------------------------
 // Axis 0 (contiguous): warp-marching kernel.
-template <typename T, class S, bool LIT>
+template <typename T, class S, int LIM, bool LIT>
 __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
+  const int lim_id = LIM >= 0 ? LIM : a.lim_id;
   using Cell = typename S::Cell;
   using Fan = typename S::Fan;
   constexpr int M = S::M;
@@ -178,7 +452,7 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
         S::for_regs(F2, [&](T& r) { r = carry[wib][lane][i++]; });
       }
       T G[M];
-      correction<S, LIT, T>(F2, F1, F, a.P, a.dtdx, a.lim_id, G);
+      correction<S, LIT, T>(F2, F1, F, a.P, a.dtdx, lim_id, G);
       T G1[M], q2[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) {
@@ -219,81 +493,6 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
 }
 
 // ---------------------------------------------------------------------------
-// Axes 1 and 2 (strided): thread-per-column marching kernel.
-template <typename T, class S, bool LIT>
-__global__ void __launch_bounds__(128) sweep_strided(const SweepArgs<T> a) {
-  using Cell = typename S::Cell;
-  using Fan = typename S::Fan;
-  constexpr int M = S::M;
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int seg = blockIdx.y;
-  const int t2 = blockIdx.z;
-
-  T smax = T(0);
-  uint32_t fin = 0xffffffffu;
-  if (x < a.n1) {
-    const int64_t off = (int64_t)x * a.t1stride + (int64_t)t2 * a.t2stride;
-    const T* qc = a.qin + off;
-    T* oc = a.qout + off;
-    const int lo = seg * a.seg_len;
-    const int hi = min(a.n, lo + a.seg_len);
-    const int64_t as = a.astride;
-
-    T qa[M];
-    load_cell<T, M>(qc, a.sstride, as, lo - 2, a, qa);
-    Cell cm1 = S::make(qa);
-    load_cell<T, M>(qc, a.sstride, as, lo - 1, a, qa);
-    Cell c0 = S::make(qa);
-    Fan Fm2 = S::solve(cm1, c0, a.P);  // F(lo-1)
-    fold_speed<S, T>(Fm2, a.P, smax);
-    load_cell<T, M>(qc, a.sstride, as, lo, a, qa);
-    Cell c1 = S::make(qa);
-    Fan Fm1 = S::solve(c0, c1, a.P);   // F(lo)
-    fold_speed<S, T>(Fm1, a.P, smax);
-    load_cell<T, M>(qc, a.sstride, as, lo + 1, a, qa);
-    Cell c2 = S::make(qa);
-    Fan F = S::solve(c1, c2, a.P);     // F(lo+1)
-    fold_speed<S, T>(F, a.P, smax);
-    T ftp[M];
-    correction<S, LIT, T>(Fm2, Fm1, F, a.P, a.dtdx, a.lim_id, ftp);  // G(lo)
-    Fm2 = Fm1;
-    Fm1 = F;
-    T qm2[M];
-#pragma unroll
-    for (int k = 0; k < M; ++k) qm2[k] = c1.q[k];
-    Cell cm = c2;
-
-    T qn[M];
-    load_cell<T, M>(qc, a.sstride, as, min(lo + 2, hi + 1), a, qn);
-    for (int i = lo + 2; i <= hi + 1; ++i) {
-      T qcur[M];
-#pragma unroll
-      for (int k = 0; k < M; ++k) qcur[k] = qn[k];
-      load_cell<T, M>(qc, a.sstride, as, min(i + 1, hi + 1), a, qn);
-      Cell ci = S::make(qcur);
-      Fan Fi = S::solve(cm, ci, a.P);
-      fold_speed<S, T>(Fi, a.P, smax);
-      T ftn[M];
-      correction<S, LIT, T>(Fm2, Fm1, Fi, a.P, a.dtdx, a.lim_id, ftn);
-      T o[M];
-      update<S, LIT, T>(qm2, Fm2, Fm1, ftn, ftp, a.P, a.dtdx, o);
-      T* dst = oc + (int64_t)(i - 2) * as;
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        dst[k * a.sstride] = o[k];
-        fin = min(fin, finite_key(o[k]));
-        ftp[k] = ftn[k];
-        qm2[k] = cm.q[k];
-      }
-      Fm2 = Fm1;
-      Fm1 = Fi;
-      cm = ci;
-    }
-  }
-  finish_block<T>(smax, fin, a);
-}
-
-// ---------------------------------------------------------------------------
 // Per-interface solve for the Riemann-plugin parity unit (riemann.py:205-223).
 template <typename T, class S>
 __global__ void solve_pairs(const T* ql, const T* qr, T* W, T* s, int64_t n, Params<T> P) {
@@ -326,9 +525,8 @@ struct GenericArgs {
   double params[4];   // already rounded to T by the host
   unsigned long long* smax_bits;
   int* nonfinite;
-  int contig;         // 1: axis 0 kernel
+  int contig;         // 1: axis-0 (x) sweep, warp-marching; 2: axis 0, TMA transpose
   int seg_len, nseg;
-  int block;          // threads per block
   int num_sms;
 };
 
@@ -348,23 +546,49 @@ inline SweepArgs<T> to_args(const GenericArgs& g) {
   return a;
 }
 
-template <typename T, class S, bool LIT>
-inline cudaError_t launch_one(const GenericArgs& g, cudaStream_t st) {
+template <typename T, class S, int LIM, bool LIT>
+inline cudaError_t launch_contig_shfl(const GenericArgs& g, cudaStream_t st) {
   SweepArgs<T> a = to_args<T>(g);
-  if (g.contig == 1) {
-    const int64_t warps = (int64_t)g.n1 * g.n2 * g.nseg;
-    const int64_t blocks = (warps + 3) / 4;
-    sweep_contig<T, S, LIT><<<(unsigned)blocks, 128, 0, st>>>(a);
-  } else {
-    dim3 grid((unsigned)((g.n1 + g.block - 1) / g.block), (unsigned)g.nseg, (unsigned)g.n2);
-    sweep_strided<T, S, LIT><<<grid, g.block, 0, st>>>(a);
-  }
+  const int64_t warps = (int64_t)g.n1 * g.n2 * g.nseg;
+  const int64_t blocks = (warps + 3) / 4;
+  sweep_contig<T, S, LIM, LIT><<<(unsigned)blocks, 128, 0, st>>>(a);
   return cudaGetLastError();
+}
+
+template <typename T, class S, int LIM, bool LIT, bool CONTIG>
+inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
+  if (CONTIG && g.contig == 1) return launch_contig_shfl<T, S, LIM, LIT>(g, st);
+  using Geo = StageGeom<T, S, CONTIG>;
+  static bool configured = false;
+  auto fn = sweep_kernel<T, S, LIM, LIT, CONTIG>;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  SweepArgs<T> a = to_args<T>(g);
+  const int64_t npen = CONTIG ? (int64_t)g.n1 * g.n2 : (int64_t)g.n1;
+  dim3 grid((unsigned)((npen + kConsumers - 1) / kConsumers), (unsigned)g.nseg,
+            CONTIG ? 1u : (unsigned)g.n2);
+  fn<<<grid, kThreads, Geo::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T, class S, bool CONTIG>
+inline cudaError_t launch_lim(const GenericArgs& g, bool literal, cudaStream_t st) {
+  if (literal) return launch_kernel<T, S, -1, true, CONTIG>(g, st);
+  switch (g.lim_id) {
+    case 0: return launch_kernel<T, S, 0, false, CONTIG>(g, st);
+    case 1: return launch_kernel<T, S, 1, false, CONTIG>(g, st);
+    case 2: return launch_kernel<T, S, 2, false, CONTIG>(g, st);
+    case 3: return launch_kernel<T, S, 3, false, CONTIG>(g, st);
+    default: return launch_kernel<T, S, 4, false, CONTIG>(g, st);
+  }
 }
 
 template <typename T, class S>
 inline cudaError_t launch_solver(const GenericArgs& g, bool literal, cudaStream_t st) {
-  return literal ? launch_one<T, S, true>(g, st) : launch_one<T, S, false>(g, st);
+  return g.contig ? launch_lim<T, S, true>(g, literal, st) : launch_lim<T, S, false>(g, literal, st);
 }
 
 template <typename T, class S>
