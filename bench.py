@@ -71,18 +71,32 @@ WORKLOADS = {
 }
 
 
-def build_inputs(name):
+def build_inputs(name, world=1, rank=0, dist=None, transport="nccl"):
+    """Workload inputs.  world > 1: weak scaling -- the slowest axis grows by
+    `world`, each rank owns one slab of the workload's size and fills only its
+    own cells (global cell centres, so every byte equals the 1-GPU layout)."""
     import paper_1805_08846_b200 as P
+    from paper_1805_08846_b200.slab import Slab
     prob, cells, lower, upper, profile, options, bc, lim, prec, label = WORKLOADS[name]
     problem = P.get_problem(prob)
+    cells = tuple(cells[:-1]) + (cells[-1] * world,)
     spec = P.GridSpec(cells, lower, upper, problem.num_states)
-    grid = P.create_grid(spec, P.grid.DTYPES[prec])
-    P.fill_initial(grid, problem.initial_profile(profile, dict(options), spec))
-    params = problem.make_params({})
-    speed = problem.speed_bound(grid, params)
     bspec = P.BoundarySpec.uniform(P.BoundaryKind(bc), problem.normal_velocity)
+    params = problem.make_params({})
+    prof = problem.initial_profile(profile, dict(options), spec)
+    slab = None
+    if world > 1:
+        slab = Slab(spec, bspec, rank, world, dist, transport=transport)
+        grid = P.create_grid(slab.local_spec, P.grid.DTYPES[prec])
+        slab.fill_initial(grid, prof)
+        speed = float(slab.allreduce_max(np.array([problem.speed_bound(grid, params)]))[0])
+    else:
+        grid = P.create_grid(spec, P.grid.DTYPES[prec])
+        P.fill_initial(grid, prof)
+        speed = problem.speed_bound(grid, params)
     return dict(P=P, problem=problem, spec=spec, grid=grid, params=params, speed=speed,
-                bspec=bspec, limiter=P.LimiterKind(lim), label=label, dtype=grid.dtype)
+                bspec=bspec, limiter=P.LimiterKind(lim), label=label, dtype=grid.dtype,
+                slab=slab, local_cells=grid.spec.num_cells)
 
 
 # ---------------------------------------------------------------------------
@@ -230,17 +244,23 @@ def flush_l2(buf):
 
 def run_gpu(args, rank, world):
     import torch
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
+    rdev = "cuda"
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.transport == "host":   # several ranks on one GPU (code-path check only)
+            tdist.init_process_group("gloo")
+            rdev = "cpu"
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
-    inp = build_inputs(args.workload)
+    inp = build_inputs(args.workload, world, rank, dist, args.transport)
     P = inp["P"]
     sim = P.Simulation(inp["grid"], inp["problem"].solver, inp["params"], inp["bspec"],
-                       limiter=inp["limiter"], initial_max_speed=inp["speed"], device=local)
+                       limiter=inp["limiter"], initial_max_speed=inp["speed"], device=local,
+                       slab=inp["slab"])
     dev = sim.device_grid
     stream = torch.cuda.current_stream()
     dev.set_stream(stream.cuda_stream)
@@ -248,7 +268,8 @@ def run_gpu(args, rank, world):
     ndim = inp["spec"].ndim
     m = inp["spec"].num_states
     isz = inp["dtype"].itemsize
-    cells = inp["spec"].num_cells
+    cells = inp["spec"].num_cells        # global cells (all ranks)
+    lcells = inp["local_cells"]
 
     for _ in range(args.warmup):
         sim.attempt_step()
@@ -276,14 +297,14 @@ def run_gpu(args, rank, world):
     ms_axis, n_axis = dev.timing()
     dev.enable_timing(False)
     if dist:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([total_ms], device=rdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = world * cells * acc / (total_ms / 1e3) / 1e9
+    value = cells * acc / (total_ms / 1e3) / 1e9
 
     # roofline: dominant kernel (largest total time)
     dom = max(range(ndim), key=lambda a: ms_axis[a])
-    bytes_per_launch = cells * m * 2 * isz
+    bytes_per_launch = lcells * m * 2 * isz
     mean_ms = ms_axis[dom] / max(n_axis[dom], 1)
     achieved = bytes_per_launch / (mean_ms / 1e3) / 1e9
     peak, peak_kind = measured_peaks()
@@ -296,8 +317,11 @@ def run_gpu(args, rank, world):
     pin_in = PinnedBuffer(inp["grid"].interior().shape, inp["dtype"])
     pin_in.array[...] = inp["grid"].interior()
     pin_out = PinnedBuffer(inp["grid"].interior().shape, inp["dtype"])
+    if inp["slab"] is not None:
+        inp["slab"].dev = None
     sim2 = P.Simulation(inp["grid"], inp["problem"].solver, inp["params"], inp["bspec"],
-                        limiter=inp["limiter"], initial_max_speed=inp["speed"], device=local)
+                        limiter=inp["limiter"], initial_max_speed=inp["speed"], device=local,
+                        slab=inp["slab"])
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -311,11 +335,11 @@ def run_gpu(args, rank, world):
     e2e_acc = sim2.steps_accepted - a0
     sim2.close()
     if dist:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=rdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     state_bytes = inp["grid"].interior().nbytes
-    e2e = {"value": world * cells * e2e_acc / e2e_s / 1e9, "unit": UNIT,
+    e2e = {"value": cells * e2e_acc / e2e_s / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": int(state_bytes / args.steps + 8),
            "d2h_bytes_per_step": int(state_bytes / args.steps + 12 * ndim)}
 
@@ -335,10 +359,13 @@ def run_gpu(args, rank, world):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": (value / PUBLISHED_SW_FP64) if is_sw64 else None,
         "dtype": "f64" if inp["dtype"] == np.float64 else "f32", "data": "synthetic",
-        "config": {"workload": inp["label"], "cells": list(inp["spec"].cells),
+        "config": {"workload": inp["label"] + (f", weak-scaled x{world} on the slowest axis"
+                                               if world > 1 else ""),
+                   "cells": list(inp["spec"].cells),
                    "steps_accepted": acc, "steps_reverted": rev,
                    "l2": "flushed between steps (256 MiB write, untimed)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"slab x{world} along the slowest axis, NCCL halo "
+                                   "exchange + max-allreduce" if world > 1 else "single GPU"),
                    "vs_baseline_ref": "CUDACLAW SW 1000^2 fp64 9.2 ms/step, C2050 (BASELINE.md)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": f"{kname} (axis {dom})",
@@ -365,6 +392,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                    help="halo transport for N>1 (host: gloo, for ranks sharing one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))

@@ -146,6 +146,12 @@ int clb_first_nonfinite(clb_handle h, int buf, int32_t *found, int32_t *state,
 int clb_halo_layout(clb_handle h, int buf, int side, void **send_ptr, void **recv_ptr,
                     size_t *block_bytes, size_t *state_stride_bytes);
 
+/* Host-staged halo transfer (the CPU-transport path of the slab exchange):
+ * to_host=1 copies the 2 owned boundary rows/planes of `side` for every
+ * state into host (m blocks of block_bytes, state-major); to_host=0 writes
+ * host into the ghost rows/planes of `side`.  Synchronous. */
+int clb_halo_copy(clb_handle h, int buf, int side, int to_host, void *host);
+
 /* Per-interface solve of n (q_l, q_r) pairs on the device (parity unit for
  * the Riemann plugins).  q arrays are (n, m) row-major in the run dtype;
  * W out (n, nw, m), s out (n, nw). */

@@ -29,7 +29,7 @@ EXPORTS = (
     "clb_create", "clb_destroy", "clb_last_error", "clb_version", "clb_set_stream",
     "clb_set_segments", "clb_upload", "clb_download", "clb_upload_padded",
     "clb_download_padded", "clb_set_boundary", "clb_sweep", "clb_sweep_async", "clb_fetch",
-    "clb_attempt_step", "clb_first_nonfinite", "clb_halo_layout", "clb_solve_pairs",
+    "clb_attempt_step", "clb_first_nonfinite", "clb_halo_layout", "clb_halo_copy", "clb_solve_pairs",
     "clb_enable_timing", "clb_timing", "clb_host_alloc", "clb_host_free", "clb_memory_info",
 )
 
@@ -92,6 +92,7 @@ def lib():
                                        ctypes.POINTER(_i64)]),
         "clb_halo_layout": (_int, [_vp, _int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                    ctypes.POINTER(_sz), ctypes.POINTER(_sz)]),
+        "clb_halo_copy": (_int, [_vp, _int, _int, _int, _vp]),
         "clb_solve_pairs": (_int, [_vp, _int, _i64, _vp, _vp, _vp, _vp]),
         "clb_enable_timing": (_int, [_vp, _int]),
         "clb_timing": (_int, [_vp, ctypes.POINTER(_dbl), ctypes.POINTER(_i64)]),
@@ -252,6 +253,18 @@ class DeviceGrid:
         _check(lib().clb_halo_layout(self.handle, buf, side, ctypes.byref(sp), ctypes.byref(rp),
                                      ctypes.byref(bb), ctypes.byref(ss)), self.handle)
         return sp.value, rp.value, bb.value, ss.value
+
+    def halo_read(self, buf: int, side: int) -> np.ndarray:
+        """The 2 owned boundary rows/planes of `side`, every state, as bytes."""
+        _, _, nbytes, _ = self.halo_layout(buf, side)
+        out = np.empty((self.num_states, nbytes), dtype=np.uint8)
+        _check(lib().clb_halo_copy(self.handle, buf, side, 1, out.ctypes.data), self.handle)
+        return out
+
+    def halo_write(self, buf: int, side: int, data: np.ndarray) -> None:
+        """Write neighbour rows into the ghost layers of `side`."""
+        a = np.ascontiguousarray(data, dtype=np.uint8)
+        _check(lib().clb_halo_copy(self.handle, buf, side, 0, a.ctypes.data), self.handle)
 
     def solve_pairs(self, axis: int, ql: np.ndarray, qr: np.ndarray, num_waves: int):
         ql = np.ascontiguousarray(ql, dtype=self.dtype)

@@ -18,14 +18,13 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libclawb200.so")
 BUILD = os.path.join(HERE, "csrc", "build")
 
-SOURCES = [
-    "clb_capi.cu",
-    "clb_inst_acoustics.cu",
-    "clb_inst_shallow_water.cu",
-    "clb_inst_advection.cu",
-    "clb_inst_vc_acoustics.cu",
+# (source, extra flags, object name): solver families compile once per dtype
+SOURCES = [("clb_capi.cu", [], "clb_capi.o")] + [
+    (f"clb_inst_{fam}.cu", [f"-DCLB_DTYPE={isz}"], f"clb_inst_{fam}_f{8 * isz}.o")
+    for fam in ("acoustics", "shallow_water", "advection", "vc_acoustics")
+    for isz in (4, 8)
 ]
-HEADERS = ["clb_solvers.cuh", "clb_kernels.cuh", "../../include/clawb200.h"]
+HEADERS = ["clb_solvers.cuh", "clb_kernels.cuh", "clb_async.cuh", "../../include/clawb200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -53,12 +52,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
     objs = []
     jobs = []
-    for src in SOURCES:
+    for src, extra, obj in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(BUILD, obj)
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [_nvcc(), *NVCC_FLAGS, "-c", s, "-o", o]
+            cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)

@@ -48,6 +48,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Producer-side wait: the producer is usually far ahead of the consumers, so
+// back off instead of spinning on issue slots the consumer warps need.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  unsigned ns = 64;
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 1024 ? 2 * ns : ns;
+  }
+}
+
 // Bulk (non-tensor) async copy global -> shared, completion on `bar`.
 // dst/src 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,

@@ -171,11 +171,26 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
     cudaEventRecord(tl.a, h->stream);
   }
   cudaError_t e;
+  const bool d64 = h->itemsize == 8;
+  const int nd = h->ndim;
+  cudaStream_t st = h->stream;
   switch (h->d.solver_id) {
-    case CLB_SOLVER_ACOUSTICS: e = clb::launch_acoustics(h->itemsize, h->ndim, axis, literal, g, h->stream); break;
-    case CLB_SOLVER_SHALLOW_WATER: e = clb::launch_shallow_water(h->itemsize, h->ndim, axis, literal, g, h->stream); break;
-    case CLB_SOLVER_ADVECTION: e = clb::launch_advection(h->itemsize, h->ndim, axis, literal, g, h->stream); break;
-    default: e = clb::launch_vc_acoustics(h->itemsize, h->ndim, axis, literal, g, h->stream); break;
+    case CLB_SOLVER_ACOUSTICS:
+      e = d64 ? clb::launch_acoustics_f64(nd, axis, literal, g, st)
+              : clb::launch_acoustics_f32(nd, axis, literal, g, st);
+      break;
+    case CLB_SOLVER_SHALLOW_WATER:
+      e = d64 ? clb::launch_shallow_water_f64(nd, axis, literal, g, st)
+              : clb::launch_shallow_water_f32(nd, axis, literal, g, st);
+      break;
+    case CLB_SOLVER_ADVECTION:
+      e = d64 ? clb::launch_advection_f64(nd, axis, literal, g, st)
+              : clb::launch_advection_f32(nd, axis, literal, g, st);
+      break;
+    default:
+      e = d64 ? clb::launch_vc_acoustics_f64(nd, axis, literal, g, st)
+              : clb::launch_vc_acoustics_f32(nd, axis, literal, g, st);
+      break;
   }
   if (e != cudaSuccess) return cuda_fail(h, e, "sweep launch");
   if (h->timing) {
@@ -546,32 +561,23 @@ int clb_memory_info(clb_handle h, size_t* device_bytes, int64_t* row_pitch) {
 
 namespace clb {
 
-template <typename T> cudaError_t pairs_acoustics(int, int, const void*, const void*, void*, void*,
-                                                  int64_t, const double*, cudaStream_t);
-template <typename T> cudaError_t pairs_shallow_water(int, const void*, const void*, void*, void*,
-                                                      int64_t, const double*, cudaStream_t);
-template <typename T> cudaError_t pairs_advection(const void*, const void*, void*, void*, int64_t,
-                                                  const double*, cudaStream_t);
-template <typename T> cudaError_t pairs_vc_acoustics(int, int, const void*, const void*, void*,
-                                                     void*, int64_t, const double*, cudaStream_t);
-
 cudaError_t pairs_dispatch(int solver, int itemsize, int ndim, int axis, const void* ql,
                            const void* qr, void* W, void* s, int64_t n, const double* p,
                            cudaStream_t st) {
   const bool d = itemsize == 8;
   switch (solver) {
     case CLB_SOLVER_ACOUSTICS:
-      return d ? pairs_acoustics<double>(ndim, axis, ql, qr, W, s, n, p, st)
-               : pairs_acoustics<float>(ndim, axis, ql, qr, W, s, n, p, st);
+      return d ? pairs_acoustics_f64(ndim, axis, ql, qr, W, s, n, p, st)
+               : pairs_acoustics_f32(ndim, axis, ql, qr, W, s, n, p, st);
     case CLB_SOLVER_SHALLOW_WATER:
-      return d ? pairs_shallow_water<double>(axis, ql, qr, W, s, n, p, st)
-               : pairs_shallow_water<float>(axis, ql, qr, W, s, n, p, st);
+      return d ? pairs_shallow_water_f64(ndim, axis, ql, qr, W, s, n, p, st)
+               : pairs_shallow_water_f32(ndim, axis, ql, qr, W, s, n, p, st);
     case CLB_SOLVER_ADVECTION:
-      return d ? pairs_advection<double>(ql, qr, W, s, n, p, st)
-               : pairs_advection<float>(ql, qr, W, s, n, p, st);
+      return d ? pairs_advection_f64(ndim, axis, ql, qr, W, s, n, p, st)
+               : pairs_advection_f32(ndim, axis, ql, qr, W, s, n, p, st);
     default:
-      return d ? pairs_vc_acoustics<double>(ndim, axis, ql, qr, W, s, n, p, st)
-               : pairs_vc_acoustics<float>(ndim, axis, ql, qr, W, s, n, p, st);
+      return d ? pairs_vc_acoustics_f64(ndim, axis, ql, qr, W, s, n, p, st)
+               : pairs_vc_acoustics_f32(ndim, axis, ql, qr, W, s, n, p, st);
   }
 }
 
@@ -592,5 +598,23 @@ extern "C" int clb_set_boundary(clb_handle h, int axis, int lo, int hi) {
     return fail(h, CLB_EINVAL, "periodic boundary must be set on both sides");
   h->d.bc[axis][0] = lo;
   h->d.bc[axis][1] = hi;
+  return CLB_OK;
+}
+
+extern "C" int clb_halo_copy(clb_handle h, int buf, int side, int to_host, void* host) {
+  if (!h || !host) return fail(h, CLB_EINVAL, "null argument");
+  void *send = nullptr, *recv = nullptr;
+  size_t bb = 0, ss = 0;
+  int r = clb_halo_layout(h, buf, side, &send, &recv, &bb, &ss);
+  if (r) return r;
+  cudaSetDevice(h->d.device);
+  for (int k = 0; k < h->M; ++k) {
+    char* hp = (char*)host + (size_t)k * bb;
+    if (to_host)
+      CLB_CUDA(h, cudaMemcpyAsync(hp, (char*)send + k * ss, bb, cudaMemcpyDeviceToHost, h->stream));
+    else
+      CLB_CUDA(h, cudaMemcpyAsync((char*)recv + k * ss, hp, bb, cudaMemcpyHostToDevice, h->stream));
+  }
+  CLB_CUDA(h, cudaStreamSynchronize(h->stream));
   return CLB_OK;
 }

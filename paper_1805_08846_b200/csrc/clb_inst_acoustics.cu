@@ -1,11 +1,20 @@
 // Instantiations: constant-coefficient acoustics (riemann.py:116-133),
 // m = ndim + 1, normal state = 1 + axis.
+// Compiled twice by build.py: -DCLB_DTYPE=4 (float) and -DCLB_DTYPE=8 (double).
 #include "clb_kernels.cuh"
+#if CLB_DTYPE == 8
+#define CLB_T double
+#define CLB_SFX(name) name##_f64
+#else
+#define CLB_T float
+#define CLB_SFX(name) name##_f32
+#endif
 
 namespace clb {
+using T = CLB_T;
 
-template <typename T>
-static cudaError_t go(int ndim, int axis, bool lit, const GenericArgs& g, cudaStream_t st) {
+cudaError_t CLB_SFX(launch_acoustics)(int ndim, int axis, bool lit, const GenericArgs& g,
+                                      cudaStream_t st) {
   if (ndim == 1) return launch_solver<T, Acoustics<T, 2, 1>>(g, lit, st);
   if (ndim == 2) {
     if (axis == 0) return launch_solver<T, Acoustics<T, 3, 1>>(g, lit, st);
@@ -16,14 +25,8 @@ static cudaError_t go(int ndim, int axis, bool lit, const GenericArgs& g, cudaSt
   return launch_solver<T, Acoustics<T, 4, 3>>(g, lit, st);
 }
 
-cudaError_t launch_acoustics(int itemsize, int ndim, int axis, bool lit, const GenericArgs& g,
-                             cudaStream_t st) {
-  return itemsize == 8 ? go<double>(ndim, axis, lit, g, st) : go<float>(ndim, axis, lit, g, st);
-}
-
-template <typename T>
-cudaError_t pairs_acoustics(int ndim, int axis, const void* ql, const void* qr, void* W, void* s,
-                            int64_t n, const double* p, cudaStream_t st) {
+cudaError_t CLB_SFX(pairs_acoustics)(int ndim, int axis, const void* ql, const void* qr, void* W,
+                                     void* s, int64_t n, const double* p, cudaStream_t st) {
   if (ndim == 1) return launch_pairs<T, Acoustics<T, 2, 1>>(ql, qr, W, s, n, p, st);
   if (ndim == 2)
     return axis == 0 ? launch_pairs<T, Acoustics<T, 3, 1>>(ql, qr, W, s, n, p, st)
@@ -32,9 +35,5 @@ cudaError_t pairs_acoustics(int ndim, int axis, const void* ql, const void* qr, 
   if (axis == 1) return launch_pairs<T, Acoustics<T, 4, 2>>(ql, qr, W, s, n, p, st);
   return launch_pairs<T, Acoustics<T, 4, 3>>(ql, qr, W, s, n, p, st);
 }
-template cudaError_t pairs_acoustics<float>(int, int, const void*, const void*, void*, void*,
-                                            int64_t, const double*, cudaStream_t);
-template cudaError_t pairs_acoustics<double>(int, int, const void*, const void*, void*, void*,
-                                             int64_t, const double*, cudaStream_t);
 
 }  // namespace clb

@@ -108,7 +108,7 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 // Resident CTAs per SM the register allocation is sized for: the fp64
 // shallow-water march needs ~150 registers (2 CTAs), everything else fits 3.
 template <typename T, class S> constexpr int kMinBlocks() {
-  return (sizeof(T) == 8 && S::NW >= 3) ? 2 : 3;
+  return (sizeof(T) == 8 && S::NW >= 3) ? 2 : (sizeof(T) == 4 ? 4 : 3);
 }
 
 template <typename T, class S, bool CONTIG> struct StageGeom {
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>()) sweep_kernel(con
       if (lane == 0) {
         for (int k = 0; k < nst; ++k) {
           const int s = k % NSTAGE;
-          if (k >= NSTAGE) mbar_wait(&empty[s], ((k / NSTAGE) - 1) & 1);
+          if (k >= NSTAGE) mbar_wait_sleep(&empty[s], ((k / NSTAGE) - 1) & 1);
           int r0 = k * NC, r1 = min(ncell, r0 + NC);
           const int rs = max(r0, 2);
           const uint32_t bytes = (r1 > rs ? (uint32_t)(r1 - rs) : 0u) * M * colbytes;
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>()) sweep_kernel(con
       }
       for (int k = 0; k < nst; ++k) {
         const int s = k % NSTAGE;
-        if (k >= NSTAGE) mbar_wait(&empty[s], ((k / NSTAGE) - 1) & 1);
+        if (k >= NSTAGE) mbar_wait_sleep(&empty[s], ((k / NSTAGE) - 1) & 1);
         if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(nvalid * M * kRowStrideContig));
         __syncwarp();
         unsigned char* st = smem + s * G::BYTES;
@@ -603,15 +603,22 @@ inline cudaError_t launch_pairs(const void* ql, const void* qr, void* W, void* s
   return cudaGetLastError();
 }
 
-// Entry points defined by the instantiation units (one per solver family).
-cudaError_t launch_acoustics(int itemsize, int ndim, int axis, bool lit, const GenericArgs& g,
-                             cudaStream_t st);
-cudaError_t launch_shallow_water(int itemsize, int ndim, int axis, bool lit,
-                                 const GenericArgs& g, cudaStream_t st);
-cudaError_t launch_advection(int itemsize, int ndim, int axis, bool lit, const GenericArgs& g,
-                             cudaStream_t st);
-cudaError_t launch_vc_acoustics(int itemsize, int ndim, int axis, bool lit,
-                                const GenericArgs& g, cudaStream_t st);
+// Entry points defined by the instantiation units (one object per solver
+// family and dtype).
+#define CLB_DECLARE_FAMILY(fam)                                                               \
+  cudaError_t launch_##fam##_f32(int ndim, int axis, bool lit, const GenericArgs& g,          \
+                                 cudaStream_t st);                                             \
+  cudaError_t launch_##fam##_f64(int ndim, int axis, bool lit, const GenericArgs& g,          \
+                                 cudaStream_t st);                                             \
+  cudaError_t pairs_##fam##_f32(int ndim, int axis, const void* ql, const void* qr, void* W,  \
+                                void* s, int64_t n, const double* p, cudaStream_t st);        \
+  cudaError_t pairs_##fam##_f64(int ndim, int axis, const void* ql, const void* qr, void* W,  \
+                                void* s, int64_t n, const double* p, cudaStream_t st);
+CLB_DECLARE_FAMILY(acoustics)
+CLB_DECLARE_FAMILY(shallow_water)
+CLB_DECLARE_FAMILY(advection)
+CLB_DECLARE_FAMILY(vc_acoustics)
+#undef CLB_DECLARE_FAMILY
 cudaError_t pairs_dispatch(int solver, int itemsize, int ndim, int axis, const void* ql,
                            const void* qr, void* W, void* s, int64_t n, const double* params,
                            cudaStream_t st);
