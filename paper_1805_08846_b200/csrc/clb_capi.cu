@@ -12,6 +12,8 @@
 // synthesised by the kernels at load time (boundary.py semantics).  Three
 // buffers per handle mirror the reference's grid + two scratch buffers
 // (timestep.py:113).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -55,6 +57,8 @@ struct clb_ctx {
   Result* h_res = nullptr;
   int num_sms = 148;
   int seg_override[3] = {0, 0, 0};
+  clb::TmaMaps maps[3][3];  // [src][dst]: load map of src, store map of dst
+  bool have_maps = false;
   bool timing = false;
   std::vector<TimedLaunch> launches;
   std::vector<cudaEvent_t> event_pool;
@@ -99,6 +103,51 @@ cudaEvent_t take_event(clb_ctx* h) {
   return e;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }();
+  return fn;
+}
+
+// 4-D view (x, y, z, state) of one buffer for the contiguous-axis sweep: box =
+// 48 bytes of x by 128 rows.  `store` limits the extent to the interior so
+// tiles that overhang the grid are clipped by the TMA unit.
+bool make_tensor_map(clb_ctx* h, int buf, bool store, void* out) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const int isz = h->itemsize;
+  cuuint64_t dims[4], strides[3];
+  if (store) {
+    dims[0] = (cuuint64_t)(h->xoff + h->cells[0]);
+    dims[1] = (cuuint64_t)(h->ndim >= 2 ? h->cells[1] + 2 : 1);
+    dims[2] = (cuuint64_t)(h->ndim == 3 ? h->cells[2] + 2 : 1);
+  } else {
+    dims[0] = (cuuint64_t)h->px;
+    dims[1] = (cuuint64_t)h->ypad;
+    dims[2] = (cuuint64_t)h->zpad;
+  }
+  dims[3] = (cuuint64_t)h->M;
+  strides[0] = (cuuint64_t)(h->ystride * isz);
+  strides[1] = (cuuint64_t)(h->zstride * isz);
+  strides[2] = (cuuint64_t)(h->sstride * isz);
+  cuuint32_t box[4] = {(cuuint32_t)(48 / isz), 128u, 1u, 1u};
+  cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+  CUresult r = enc((CUtensorMap*)out,
+                   isz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                   h->buf[buf], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Geometry of one sweep: which kernel, extents and strides.
 clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   clb::GenericArgs g;
@@ -118,16 +167,26 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   // segment re-reads 4 cells and re-solves 3 fans of its neighbour).
   const int64_t target_ctas = (int64_t)h->num_sms * 6;
   int64_t pen_ctas;
-  static const int contig_mode = [] {
+  // x-sweep kernel: the TMA tensor-map variant wins when the march is
+  // compute-heavy (fp64 shallow water, profiles/r1_notes.md); the warp-shuffle
+  // variant wins elsewhere.  CLB_CONTIG=tma|shfl overrides.
+  static const int contig_env = [] {
     const char* e = getenv("CLB_CONTIG");
-    return (e && e[0] == 't') ? 2 : 1;
+    return e ? (e[0] == 't' ? 2 : 1) : 0;
   }();
+  const int contig_mode = contig_env ? contig_env
+                          : ((h->d.solver_id == CLB_SOLVER_SHALLOW_WATER && h->itemsize == 8) ? 2 : 1);
   if (axis == 0) {
-    g.contig = contig_mode;
+    g.contig = (contig_mode == 2 && h->have_maps) ? 2 : 1;
     g.n = (int)nx; g.n1 = (int)ny; g.n2 = (int)nz;
     g.astride = 1; g.t1stride = h->ystride; g.t2stride = h->zstride;
-    // warp-marching: one warp per (row, segment), 4 warps per CTA
-    pen_ctas = contig_mode == 1 ? (ny * nz + 3) / 4 : (ny * nz + 127) / 128;
+    g.maps = &h->maps[src][dst];
+    g.tx0 = (int)h->xoff;
+    g.ty0 = h->ndim >= 2 ? 2 : 0;
+    g.tz0 = h->ndim == 3 ? 2 : 0;
+    // warp-marching: one warp per (row, segment), 4 warps per CTA;
+    // TMA: 128 rows of one z-plane per CTA
+    pen_ctas = g.contig == 1 ? (ny * nz + 3) / 4 : ((ny + 127) / 128) * nz;
   } else {
     g.contig = 0;
     g.n1 = (int)nx;
@@ -140,7 +199,7 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
     pen_ctas = ((nx + 127) / 128) * g.n2;
   }
   // contig stages are 48 bytes of a row: segment starts must stay aligned
-  const int64_t align = (axis == 0 && contig_mode == 2) ? 48 / h->itemsize : 1;
+  const int64_t align = (axis == 0 && g.contig == 2) ? 48 / h->itemsize : 1;
   int64_t nseg = (target_ctas + pen_ctas - 1) / pen_ctas;
   nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, g.n / 32));
   int64_t L = (g.n + nseg - 1) / nseg;
@@ -307,6 +366,12 @@ int clb_create(const clb_desc* desc, clb_handle* out) {
     }
     cudaMemsetAsync(h->buf[i], 0, h->buf_bytes, h->stream);
   }
+  h->have_maps = true;
+  for (int sb = 0; sb < 3 && h->have_maps; ++sb)
+    for (int db = 0; db < 3; ++db)
+      if (sb != db && !(make_tensor_map(h, sb, false, h->maps[sb][db].ld) &&
+                        make_tensor_map(h, db, true, h->maps[sb][db].st)))
+        h->have_maps = false;
   e = cudaMalloc(&h->d_res, sizeof(Result));
   if (e == cudaSuccess) e = cudaMallocHost(&h->h_res, sizeof(Result));
   if (e == cudaSuccess) e = cudaMemsetAsync(h->d_res, 0, sizeof(Result), h->stream);

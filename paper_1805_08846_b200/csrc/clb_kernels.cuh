@@ -57,6 +57,14 @@ template <typename T> struct SweepArgs {
   Params<T> P;
   unsigned long long* smax_bits;
   int* nonfinite;
+  int tx0, ty0, tz0;  // tensor-map coordinates of interior cell (0,0,0)
+};
+
+// TMA descriptors of the source (load) and destination (store) buffers of a
+// contiguous-axis sweep, passed by value as a __grid_constant__ parameter.
+struct TmaMaps {
+  alignas(64) unsigned char ld[128];
+  alignas(64) unsigned char st[128];
 };
 
 // boundary.py:108-122 as a read-side index map: ghost cell j of a pencil
@@ -115,9 +123,15 @@ template <typename T, class S, bool CONTIG> struct StageGeom {
   static constexpr int NC = CONTIG ? (kRowStrideContig / (int)sizeof(T)) : 3;  // cells/stage
   static constexpr int BYTES = CONTIG ? S::M * kConsumers * kRowStrideContig
                                       : S::M * NC * kConsumers * (int)sizeof(T);
-  static constexpr int NSTAGE = (72 * 1024 / BYTES) < 2 ? 2
-                                : ((72 * 1024 / BYTES) > 6 ? 6 : (72 * 1024 / BYTES));
-  static constexpr int SMEM = NSTAGE * BYTES + 2 * NSTAGE * 8;
+  // two leading alignment dummies: the prologue cells sit at r = 2..5, so every
+  // 3-cell group starts on ring phase 0, and every contig stage box starts
+  // 16-byte aligned (TMA requirement) because segments start at multiples of NC.
+  static constexpr int A = 2;
+  static constexpr int NSTAGE_RAW = CONTIG ? (S::M >= 4 ? 2 : 3) : (72 * 1024 / BYTES);
+  static constexpr int NSTAGE = NSTAGE_RAW < 2 ? 2 : (NSTAGE_RAW > 6 ? 6 : NSTAGE_RAW);
+  static constexpr int NOUT = CONTIG ? 2 : 0;  // output staging tiles (TMA store)
+  static constexpr int SMEM = (NSTAGE + NOUT) * BYTES + 2 * NSTAGE * 8;
+  static_assert(A % 3 == 2, "prologue phase");
 };
 
 // ---------------------------------------------------------------------------
@@ -160,15 +174,16 @@ template <typename T, class S, int LIM, bool LIT> struct March {
 };
 
 // ---------------------------------------------------------------------------
-// The sweep kernel.  Relative cell index r = 0 .. L+5 of a segment [lo, hi)
-// maps to pencil cell j = lo - 4 + r: r = 0, 1 are alignment dummies, r = 2..5
-// the prologue (cells lo-2 .. lo+1), r >= 6 emits cell lo + r - 6.
+// The sweep kernel.  Relative cell index r = 0 .. L+A+3 of a segment [lo, hi)
+// maps to pencil cell j = lo - 2 - A + r: r < A are alignment dummies, r =
+// A..A+3 the prologue (cells lo-2 .. lo+1), r >= A+4 emits cell lo + r - A - 4.
 template <typename T, class S, int LIM, bool LIT, bool CONTIG>
-__global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>()) sweep_kernel(const SweepArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
+    sweep_kernel(const SweepArgs<T> a, const __grid_constant__ TmaMaps maps) {
   using G = StageGeom<T, S, CONTIG>;
-  constexpr int NC = G::NC, NSTAGE = G::NSTAGE, M = S::M;
+  constexpr int NC = G::NC, NSTAGE = G::NSTAGE, M = S::M, A = G::A;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * G::BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (NSTAGE + G::NOUT) * G::BYTES);
   uint64_t* empty = full + NSTAGE;
 
   const int tid = threadIdx.x;
@@ -176,11 +191,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>()) sweep_kernel(con
   const int seg = blockIdx.y;
   const int lo = seg * a.seg_len;
   const int hi = min(a.n, lo + a.seg_len);
-  const int ncell = hi - lo + 6;
+  const int ncell = hi - lo + A + 4;
   const int nst = (ncell + NC - 1) / NC;
-  // pencil block
+  // pencil block: strided -> 128 x-columns at transverse index blockIdx.z;
+  // contig -> 128 rows (y) of plane z = blockIdx.z
   const int64_t pb = (int64_t)blockIdx.x * kConsumers;
-  const int64_t npen = CONTIG ? (int64_t)a.n1 * a.n2 : (int64_t)a.n1;
+  const int64_t npen = a.n1;
   const int nvalid = (int)(npen - pb < (int64_t)kConsumers ? npen - pb : (int64_t)kConsumers);
 
   if (tid == 0) {
@@ -198,22 +214,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>()) sweep_kernel(con
   if (warp == kConsumers / 32) {
     // ------------------------------ producer ------------------------------
     constexpr int isz = (int)sizeof(T);
-    if (!CONTIG) {
-      const int64_t x0 = pb;
-      const uint32_t colbytes = (uint32_t)(((nvalid * isz) + 15) & ~15);
-      const T* base = a.qin + x0 + (int64_t)blockIdx.z * a.t2stride;
-      if (lane == 0) {
+    if (lane == 0) {
+      if (!CONTIG) {
+        const uint32_t colbytes = (uint32_t)(((nvalid * isz) + 15) & ~15);
+        const T* base = a.qin + pb + (int64_t)blockIdx.z * a.t2stride;
         for (int k = 0; k < nst; ++k) {
           const int s = k % NSTAGE;
           if (k >= NSTAGE) mbar_wait_sleep(&empty[s], ((k / NSTAGE) - 1) & 1);
-          int r0 = k * NC, r1 = min(ncell, r0 + NC);
-          const int rs = max(r0, 2);
+          const int r0 = k * NC, r1 = min(ncell, r0 + NC);
+          const int rs = max(r0, A);
           const uint32_t bytes = (r1 > rs ? (uint32_t)(r1 - rs) : 0u) * M * colbytes;
           mbar_arrive_expect_tx(&full[s], bytes);
           unsigned char* st = smem + s * G::BYTES;
           for (int r = rs; r < r1; ++r) {
             bool neg;
-            const int js = remap(lo - 4 + r, a.n, a.bc_lo, a.bc_hi, neg);
+            const int js = remap(lo - 2 - A + r, a.n, a.bc_lo, a.bc_hi, neg);
             const T* src = base + (int64_t)js * a.astride;
 #pragma unroll
             for (int q = 0; q < M; ++q)
@@ -221,32 +236,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>()) sweep_kernel(con
                        colbytes, &full[s]);
           }
         }
-      }
-    } else {
-      // rows owned by this lane: lane, lane+32, lane+64, lane+96
-      const T* rowp[4];
+      } else {
+        const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
+        for (int k = 0; k < nst; ++k) {
+          const int s = k % NSTAGE;
+          if (k >= NSTAGE) mbar_wait_sleep(&empty[s], ((k / NSTAGE) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], (uint32_t)G::BYTES);
+          unsigned char* st = smem + s * G::BYTES;
+          const int cx = a.tx0 + lo - 2 - A + k * NC;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t R = pb + lane + 32 * u;
-        const int y = (int)(R % a.n1), z = (int)(R / a.n1);
-        rowp[u] = a.qin + (int64_t)y * a.t1stride + (int64_t)z * a.t2stride;
-      }
-      for (int k = 0; k < nst; ++k) {
-        const int s = k % NSTAGE;
-        if (k >= NSTAGE) mbar_wait_sleep(&empty[s], ((k / NSTAGE) - 1) & 1);
-        if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(nvalid * M * kRowStrideContig));
-        __syncwarp();
-        unsigned char* st = smem + s * G::BYTES;
-        const int x = lo - 4 + k * NC;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int t = lane + 32 * u;
-          if (t < nvalid) {
-#pragma unroll
-            for (int q = 0; q < M; ++q)
-              bulk_g2s(st + (q * kConsumers + t) * kRowStrideContig, rowp[u] + q * a.sstride + x,
-                       kRowStrideContig, &full[s]);
-          }
+          for (int q = 0; q < M; ++q)
+            tma_load_4d(st + q * kConsumers * kRowStrideContig, maps.ld, cx, cy, cz, q, &full[s]);
         }
       }
     }
@@ -257,28 +257,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>()) sweep_kernel(con
     March<T, S, LIM, LIT> mr;
     mr.smax = T(0);
     mr.fin = 0xffffffffu;
-    // pencil addressing for stores / ghost loads
     const T* pin;
     T* pout;
-    int64_t step_el;
     if (CONTIG) {
-      const int64_t R = pb + (active ? t : 0);
-      const int y = (int)(R % a.n1), z = (int)(R / a.n1);
-      const int64_t off = (int64_t)y * a.t1stride + (int64_t)z * a.t2stride;
+      const int64_t off = (pb + (active ? t : 0)) * a.t1stride + (int64_t)blockIdx.z * a.t2stride;
       pin = a.qin + off;
       pout = a.qout + off;
-      step_el = 1;
     } else {
       const int64_t off = pb + (active ? t : 0) + (int64_t)blockIdx.z * a.t2stride;
       pin = a.qin + off;
       pout = a.qout + off;
-      step_el = a.astride;
     }
     const bool halo_lo = a.bc_lo == BC_HALO, halo_hi = a.bc_hi == BC_HALO;
     const bool refl_lo = a.bc_lo == BC_REFLECTIVE, refl_hi = a.bc_hi == BC_REFLECTIVE;
+    unsigned char* outs = smem + NSTAGE * G::BYTES;  // contig output tiles
 
     auto fetch = [&](const unsigned char* st, int r, int c, T (&q)[M]) {
-      const int j = lo - 4 + r;
+      const int j = lo - 2 - A + r;
       if (!CONTIG) {
 #pragma unroll
         for (int k = 0; k < M; ++k)
@@ -309,13 +304,51 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>()) sweep_kernel(con
         }
       }
     };
-    auto emit = [&](int r, const T (&o)[M]) {
-      T* dst = pout + (int64_t)(lo + r - 6) * step_el;
+    // emit the updated cell e = r - A - 4 of the segment (cell lo + e).  Contig
+    // sweeps stage it in output tile e / NC (double-buffered) for a TMA store.
+    auto emit = [&](int k, int r, int c, bool valid, const T (&o)[M]) {
+      (void)k;
+      (void)c;
+      if (CONTIG) {
+        const int e = r - A - 4;
+        unsigned char* ob = outs + ((e / NC) & 1) * G::BYTES;
 #pragma unroll
-      for (int k = 0; k < M; ++k) {
-        dst[k * a.sstride] = o[k];
-        mr.fin = min(mr.fin, finite_key(o[k]));
+        for (int q = 0; q < M; ++q)
+          *reinterpret_cast<T*>(ob + (q * kConsumers + t) * kRowStrideContig +
+                                (e % NC) * (int)sizeof(T)) = o[q];
+        if (valid && active) {
+#pragma unroll
+          for (int q = 0; q < M; ++q) mr.fin = min(mr.fin, finite_key(o[q]));
+        }
+      } else if (valid && active) {
+        T* dst = pout + (int64_t)(lo + r - A - 4) * a.astride;
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          dst[q * a.sstride] = o[q];
+          mr.fin = min(mr.fin, finite_key(o[q]));
+        }
       }
+    };
+
+    // output tile `tile` complete in smem -> one TMA tensor store per state.
+    // Before the barrier, thread 0 makes sure the store of tile-2 (issued at
+    // the previous flush or earlier) has finished reading the buffer tile+1
+    // is about to be written into.
+    int flushed = -1;
+    auto flush = [&](int tile) {
+      fence_proxy_async_smem();
+      if (t == 0) bulk_wait_read<0>();
+      named_barrier_sync(1, kConsumers);
+      if (t == 0) {
+        const unsigned char* ob = outs + (tile & 1) * G::BYTES;
+        const int cx = a.tx0 + lo + tile * NC;
+        const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
+#pragma unroll
+        for (int q = 0; q < M; ++q)
+          tma_store_4d(maps.st, ob + q * kConsumers * kRowStrideContig, cx, cy, cz, q);
+        bulk_commit();
+      }
+      flushed = tile;
     };
 
     for (int k = 0; k < nst; ++k) {
@@ -328,35 +361,42 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>()) sweep_kernel(con
         if (r0 >= ncell) break;
         const int c0 = 3 * g;
         T q[M];
-        if (r0 >= 6) {
+        if (r0 >= A + 4) {
           T o[M];
           bool v;
-          fetch(st, r0, c0, q);
           v = r0 < ncell;
+          fetch(st, r0, c0, q);
           mr.template step<0>(q, a, v && active, o);
-          if (v && active) emit(r0, o);
-          fetch(st, r0 + 1, c0 + 1, q);
+          emit(k, r0, c0, v, o);
           v = r0 + 1 < ncell;
+          fetch(st, r0 + 1, c0 + 1, q);
           mr.template step<1>(q, a, v && active, o);
-          if (v && active) emit(r0 + 1, o);
-          fetch(st, r0 + 2, c0 + 2, q);
+          emit(k, r0 + 1, c0 + 1, v, o);
           v = r0 + 2 < ncell;
+          fetch(st, r0 + 2, c0 + 2, q);
           mr.template step<2>(q, a, v && active, o);
-          if (v && active) emit(r0 + 2, o);
-        } else if (r0 == 3) {
-          fetch(st, 3, c0, q);
+          emit(k, r0 + 2, c0 + 2, v, o);
+          // the group's last cell closes an output tile every NC cells
+          if (CONTIG && (r0 + 2 - A - 4) % NC == NC - 1) flush((r0 + 2 - A - 4) / NC);
+        } else if (r0 == A + 1) {
+          fetch(st, r0, c0, q);
           mr.template fan<0>(q, a, active);          // F(lo-1)
-          fetch(st, 4, c0 + 1, q);
+          fetch(st, r0 + 1, c0 + 1, q);
           mr.template fan<1>(q, a, active);          // F(lo)
-          fetch(st, 5, c0 + 2, q);
+          fetch(st, r0 + 2, c0 + 2, q);
           mr.template fan_corr<2>(q, a, active);     // F(lo+1), G(lo)
-        } else {
-          fetch(st, 2, c0 + 2, q);
+        } else if (r0 == A - 2) {
+          fetch(st, r0 + 2, c0 + 2, q);
           mr.template first<2>(q);                   // cell lo-2
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (CONTIG) {
+      const int last = (ncell - 1 - A - 4) / NC;  // tile of the segment's last cell
+      if (last > flushed) flush(last);
+      if (t == 0) bulk_wait<0>();
     }
     smax = mr.smax;
     fin = mr.fin;
@@ -516,6 +556,8 @@ __global__ void solve_pairs(const T* ql, const T* qr, T* W, T* s, int64_t n, Par
 // Launch plumbing shared by the instantiation units.
 
 struct GenericArgs {
+  const TmaMaps* maps;  // contig TMA sweep only
+  int tx0, ty0, tz0;
   const void* qin;
   void* qout;
   int64_t sstride, astride, t1stride, t2stride;
@@ -543,6 +585,7 @@ inline SweepArgs<T> to_args(const GenericArgs& g) {
   for (int i = 0; i < 4; ++i) a.P.p[i] = (T)g.params[i];
   a.smax_bits = g.smax_bits;
   a.nonfinite = g.nonfinite;
+  a.tx0 = g.tx0; a.ty0 = g.ty0; a.tz0 = g.tz0;
   return a;
 }
 
@@ -567,10 +610,9 @@ inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
     configured = true;
   }
   SweepArgs<T> a = to_args<T>(g);
-  const int64_t npen = CONTIG ? (int64_t)g.n1 * g.n2 : (int64_t)g.n1;
-  dim3 grid((unsigned)((npen + kConsumers - 1) / kConsumers), (unsigned)g.nseg,
-            CONTIG ? 1u : (unsigned)g.n2);
-  fn<<<grid, kThreads, Geo::SMEM, st>>>(a);
+  static const TmaMaps none{};
+  dim3 grid((unsigned)((g.n1 + kConsumers - 1) / kConsumers), (unsigned)g.nseg, (unsigned)g.n2);
+  fn<<<grid, kThreads, Geo::SMEM, st>>>(a, CONTIG ? *g.maps : none);
   return cudaGetLastError();
 }
 
