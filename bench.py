@@ -262,7 +262,10 @@ def run_gpu(args, rank, world):
                        limiter=inp["limiter"], initial_max_speed=inp["speed"], device=local,
                        slab=inp["slab"])
     dev = sim.device_grid
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy) stream: the library maps handle 0 to its own stream,
+    # so the L2 flush, the step events and the sweeps must share this one
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     dev.set_stream(stream.cuda_stream)
     flush = torch.empty(1024 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     ndim = inp["spec"].ndim

@@ -158,6 +158,16 @@ int clb_halo_copy(clb_handle h, int buf, int side, int to_host, void *host);
 int clb_solve_pairs(clb_handle h, int axis, int64_t n, const void *ql, const void *qr,
                     void *W, void *s);
 
+/* Self-test of the branch-free fp64 division / square root used by the
+ * sweep kernels (clb_solvers.cuh FastArith) against div.rn.f64 /
+ * sqrt.rn.f64 on n host pairs (a[i], b[i]) on device `device`.  out[0] =
+ * quotients where the fast path claimed validity but differs bitwise from
+ * div.rn, out[1] = same for sqrt(a[i]), out[2] / out[3] = how many
+ * quotients / roots fell back to the exact path; out[4..7] the same for the
+ * fp32 path on the low 32 bits of a[i], b[i] read as floats.  No handle
+ * needed. */
+int clb_selftest_arith(int device, int64_t n, const double *a, const double *b, int64_t out[8]);
+
 /* Kernel timing (CUDA events on the launch stream) for the bench: when
  * enabled, every sweep launch is bracketed by events; clb_timing returns
  * the summed milliseconds and launch counts per axis and resets them. */

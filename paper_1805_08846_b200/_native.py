@@ -14,7 +14,10 @@ import numpy as np
 from .errors import DeviceError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libclawb200.so")
+#: CLB_LIB_VARIANT=<tag> loads libclawb200_<tag>.so (tuning experiments built
+#: by `python -m paper_1805_08846_b200.build --variant <tag> -D...`)
+_VARIANT = os.environ.get("CLB_LIB_VARIANT")
+LIB_PATH = os.path.join(HERE, f"libclawb200_{_VARIANT}.so" if _VARIANT else "libclawb200.so")
 
 CLB_OK = 0
 CLB_EINVAL = -1
@@ -31,6 +34,7 @@ EXPORTS = (
     "clb_download_padded", "clb_set_boundary", "clb_sweep", "clb_sweep_async", "clb_fetch",
     "clb_attempt_step", "clb_first_nonfinite", "clb_halo_layout", "clb_halo_copy", "clb_solve_pairs",
     "clb_enable_timing", "clb_timing", "clb_host_alloc", "clb_host_free", "clb_memory_info",
+    "clb_selftest_arith",
 )
 
 
@@ -99,6 +103,7 @@ def lib():
         "clb_host_alloc": (_vp, [_sz]),
         "clb_host_free": (None, [_vp]),
         "clb_memory_info": (_int, [_vp, ctypes.POINTER(_sz), ctypes.POINTER(_i64)]),
+        "clb_selftest_arith": (_int, [_int, _i64, _vp, _vp, ctypes.POINTER(_i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -290,6 +295,19 @@ class DeviceGrid:
         p = _i64()
         _check(lib().clb_memory_info(self.handle, ctypes.byref(b), ctypes.byref(p)), self.handle)
         return b.value, p.value
+
+
+def selftest_arith(a, b, device: int = 0):
+    """Branch-free div/sqrt of the sweep kernels vs div.rn/sqrt.rn on the
+    device: (div mismatches, sqrt mismatches, div fallbacks, sqrt fallbacks)
+    for fp64, then the same four for fp32 (low words of a, b as floats)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError("a and b must have the same shape")
+    out = (_i64 * 8)()
+    _check(lib().clb_selftest_arith(device, a.size, a.ctypes.data, b.ctypes.data, out))
+    return tuple(int(out[i]) for i in range(8))
 
 
 class PinnedBuffer:

@@ -47,17 +47,23 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, variant: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile and link the library; `variant` + `defines` build a tuning
+    variant libclawb200_<variant>.so from its own object directory."""
+    out = OUT if not variant else os.path.join(HERE, f"libclawb200_{variant}.so")
+    bdir = BUILD if not variant else os.path.join(CSRC, f"build_{variant}")
+    extra_d = [f"-D{d}" for d in defines]
+    os.makedirs(bdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
     objs = []
     jobs = []
     for src, extra, obj in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, obj)
+        o = os.path.join(bdir, obj)
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-c", s, "-o", o]
+            cmd = [_nvcc(), *NVCC_FLAGS, *extra, *extra_d, "-c", s, "-o", o]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)
@@ -73,13 +79,20 @@ def build(verbose: bool = False, force: bool = False) -> str:
                     sys.stderr.write(r.stdout + r.stderr)
                 if r.returncode != 0:
                     raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
-    if force or _stale(OUT, objs):
-        cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", OUT, *objs]
+    if force or _stale(out, objs):
+        cmd = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {r.stdout}{r.stderr}")
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("-f", action="store_true")
+    ap.add_argument("--variant")
+    ap.add_argument("-D", action="append", default=[])
+    a = ap.parse_args()
+    print(build(verbose=a.v, force=a.f, variant=a.variant, defines=tuple(a.D)))

@@ -31,14 +31,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// try_wait with a suspend-time hint: the warp is parked in hardware until
+// the phase completes (or the hint expires) instead of spinning on issue
+// slots the marching warps need.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
       : "memory");
   return ok != 0;
 }
@@ -48,14 +51,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// Producer-side wait: the producer is usually far ahead of the consumers, so
-// back off instead of spinning on issue slots the consumer warps need.
+// Producer-side wait (kept as a separate name: the producer runs ahead).
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  unsigned ns = 64;
-  while (!mbar_try_wait(bar, parity)) {
-    __nanosleep(ns);
-    ns = ns < 1024 ? 2 * ns : ns;
-  }
+  mbar_wait(bar, parity);
 }
 
 // Bulk (non-tensor) async copy global -> shared, completion on `bar`.

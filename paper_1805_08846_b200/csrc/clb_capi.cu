@@ -294,6 +294,32 @@ __global__ void first_bad_kernel(const T* q, int64_t sstride, int64_t ystride, i
 
 }  // namespace
 
+
+// FastArith (clb_solvers.cuh) against div.rn / sqrt.rn, bit for bit.
+__global__ void selftest_arith_kernel(const double* a, const double* b, int64_t n,
+                                      unsigned long long* cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = a[i], y = b[i];
+  bool bq = false, bs = false;
+  const double qf = clb::FastArith::div<double, clb::kChkAll>(x, y, bq);
+  const double sf = clb::FastArith::sqrt<double>(x, bs);
+  const double qr = __ddiv_rn(x, y), sr = __dsqrt_rn(x);
+  if (!bq && __double_as_longlong(qf) != __double_as_longlong(qr)) atomicAdd(&cnt[0], 1ull);
+  if (!bs && __double_as_longlong(sf) != __double_as_longlong(sr)) atomicAdd(&cnt[1], 1ull);
+  if (bq) atomicAdd(&cnt[2], 1ull);
+  if (bs) atomicAdd(&cnt[3], 1ull);
+  // fp32: the low words reinterpreted as floats (every float class occurs)
+  const float xf = __int_as_float(__double2loint(x)), yf = __int_as_float(__double2loint(y));
+  bool cq = false, cs = false;
+  const float qff = clb::FastArith::div<float, clb::kChkAll>(xf, yf, cq);
+  const float sff = clb::FastArith::sqrt<float>(xf, cs);
+  if (!cq && __float_as_int(qff) != __float_as_int(__fdiv_rn(xf, yf))) atomicAdd(&cnt[4], 1ull);
+  if (!cs && __float_as_int(sff) != __float_as_int(__fsqrt_rn(xf))) atomicAdd(&cnt[5], 1ull);
+  if (cq) atomicAdd(&cnt[6], 1ull);
+  if (cs) atomicAdd(&cnt[7], 1ull);
+}
+
 extern "C" {
 
 int clb_version(void) { return 1; }
@@ -580,6 +606,32 @@ int clb_solve_pairs(clb_handle h, int axis, int64_t n, const void* ql, const voi
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   cudaFree(d);
   if (e != cudaSuccess) return cuda_fail(h, e, "solve_pairs");
+  return CLB_OK;
+}
+
+int clb_selftest_arith(int device, int64_t n, const double* a, const double* b, int64_t out[8]) {
+  if (!a || !b || !out || n < 0) return fail(nullptr, CLB_EINVAL, "null argument");
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  if (n == 0) return CLB_OK;
+  if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, CLB_ECUDA, "no such device");
+  double* d = nullptr;
+  unsigned long long* cnt = nullptr;
+  const size_t nb = (size_t)n * sizeof(double);
+  cudaError_t e = cudaMalloc(&d, 2 * nb);
+  if (e == cudaSuccess) e = cudaMalloc(&cnt, 8 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(cnt, 0, 8 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemcpy(d, a, nb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d + n, b, nb, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    selftest_arith_kernel<<<(unsigned)((n + 255) / 256), 256>>>(d, d + n, n, cnt);
+    e = cudaGetLastError();
+  }
+  unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpy(h, cnt, sizeof(h), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  cudaFree(cnt);
+  if (e != cudaSuccess) return fail(nullptr, CLB_ECUDA, cudaGetErrorString(e));
+  for (int i = 0; i < 8; ++i) out[i] = (int64_t)h[i];
   return CLB_OK;
 }
 

@@ -113,10 +113,13 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
   }
 }
 
+#ifndef CLB_SW_MINB
+#define CLB_SW_MINB 2
+#endif
 // Resident CTAs per SM the register allocation is sized for: the fp64
 // shallow-water march needs ~150 registers (2 CTAs), everything else fits 3.
 template <typename T, class S> constexpr int kMinBlocks() {
-  return (sizeof(T) == 8 && S::NW >= 3) ? 2 : (sizeof(T) == 4 ? 4 : 3);
+  return (sizeof(T) == 8 && S::NW >= 3) ? CLB_SW_MINB : (sizeof(T) == 4 ? 4 : 3);
 }
 
 template <typename T, class S, bool CONTIG> struct StageGeom {
@@ -136,8 +139,9 @@ template <typename T, class S, bool CONTIG> struct StageGeom {
 
 // ---------------------------------------------------------------------------
 // The ring-march state of one pencil.  Slot p holds interface/cell index
-// i with i % 3 == p; P is the slot of the incoming cell.
-template <typename T, class S, int LIM, bool LIT> struct March {
+// i with i % 3 == p; P is the slot of the incoming cell.  D is the arithmetic
+// policy (clb_solvers.cuh); `bad` collects FastArith domain failures.
+template <typename T, class S, int LIM, bool LIT, class D> struct March {
   using Cell = typename S::Cell;
   using Fan = typename S::Fan;
   static constexpr int M = S::M;
@@ -146,23 +150,26 @@ template <typename T, class S, int LIM, bool LIT> struct March {
   T G[3][M];
   T smax;
   uint32_t fin;
+  bool bad;
 
   __device__ __forceinline__ int lim(const SweepArgs<T>& a) const { return LIM >= 0 ? LIM : a.lim_id; }
 
   // prologue steps (no output)
-  template <int P> __device__ __forceinline__ void first(const T (&q)[M]) { X[P] = S::make(q); }
+  template <int P> __device__ __forceinline__ void first(const T (&q)[M]) {
+    X[P] = S::template make<D>(q, bad);
+  }
   template <int P> __device__ __forceinline__ void fan(const T (&q)[M], const SweepArgs<T>& a,
                                                        bool fold) {
     constexpr int P1 = (P + 2) % 3;
-    X[P] = S::make(q);
-    F[P] = S::solve(X[P1], X[P], a.P);
+    X[P] = S::template make<D>(q, bad);
+    F[P] = S::template solve<D>(X[P1], X[P], a.P, bad);
     if (fold) fold_speed<S, T>(F[P], a.P, smax);
   }
   template <int P> __device__ __forceinline__ void fan_corr(const T (&q)[M],
                                                             const SweepArgs<T>& a, bool fold) {
     constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
     fan<P>(q, a, fold);
-    correction<S, LIT, T>(F[P2], F[P1], F[P], a.P, a.dtdx, lim(a), G[P1]);
+    correction<S, LIT, D, T>(F[P2], F[P1], F[P], a.P, a.dtdx, lim(a), G[P1], bad);
   }
   // steady step: returns the updated cell i-2 in `out`
   template <int P> __device__ __forceinline__ void step(const T (&q)[M], const SweepArgs<T>& a,
@@ -174,18 +181,16 @@ template <typename T, class S, int LIM, bool LIT> struct March {
 };
 
 // ---------------------------------------------------------------------------
-// The sweep kernel.  Relative cell index r = 0 .. L+A+3 of a segment [lo, hi)
-// maps to pencil cell j = lo - 2 - A + r: r < A are alignment dummies, r =
-// A..A+3 the prologue (cells lo-2 .. lo+1), r >= A+4 emits cell lo + r - A - 4.
-template <typename T, class S, int LIM, bool LIT, bool CONTIG>
-__global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
-    sweep_kernel(const SweepArgs<T> a, const __grid_constant__ TmaMaps maps) {
+// One pass of a CTA over its segment: the producer warp streams the stages,
+// the consumer warps march.  k0 numbers the pass's first stage in the CTA's
+// running stage sequence (mbarrier phases continue across passes).  Returns
+// the consumer's (smax, fin, bad) in the references.
+template <typename T, class S, int LIM, bool LIT, bool CONTIG, class D>
+__device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const TmaMaps& maps,
+                                             unsigned char* smem, uint64_t* full, uint64_t* empty,
+                                             int k0, T& smax, uint32_t& fin, bool& bad) {
   using G = StageGeom<T, S, CONTIG>;
   constexpr int NC = G::NC, NSTAGE = G::NSTAGE, M = S::M, A = G::A;
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (NSTAGE + G::NOUT) * G::BYTES);
-  uint64_t* empty = full + NSTAGE;
-
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int seg = blockIdx.y;
@@ -199,18 +204,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
   const int64_t npen = a.n1;
   const int nvalid = (int)(npen - pb < (int64_t)kConsumers ? npen - pb : (int64_t)kConsumers);
 
-  if (tid == 0) {
-    for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers / 32);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  T smax = T(0);
-  uint32_t fin = 0xffffffffu;
-
   if (warp == kConsumers / 32) {
     // ------------------------------ producer ------------------------------
     constexpr int isz = (int)sizeof(T);
@@ -219,8 +212,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
         const uint32_t colbytes = (uint32_t)(((nvalid * isz) + 15) & ~15);
         const T* base = a.qin + pb + (int64_t)blockIdx.z * a.t2stride;
         for (int k = 0; k < nst; ++k) {
-          const int s = k % NSTAGE;
-          if (k >= NSTAGE) mbar_wait_sleep(&empty[s], ((k / NSTAGE) - 1) & 1);
+          const int kk = k0 + k;
+          const int s = kk % NSTAGE;
+          if (kk >= NSTAGE) mbar_wait_sleep(&empty[s], ((kk / NSTAGE) - 1) & 1);
           const int r0 = k * NC, r1 = min(ncell, r0 + NC);
           const int rs = max(r0, A);
           const uint32_t bytes = (r1 > rs ? (uint32_t)(r1 - rs) : 0u) * M * colbytes;
@@ -239,8 +233,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
       } else {
         const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
         for (int k = 0; k < nst; ++k) {
-          const int s = k % NSTAGE;
-          if (k >= NSTAGE) mbar_wait_sleep(&empty[s], ((k / NSTAGE) - 1) & 1);
+          const int kk = k0 + k;
+          const int s = kk % NSTAGE;
+          if (kk >= NSTAGE) mbar_wait_sleep(&empty[s], ((kk / NSTAGE) - 1) & 1);
           mbar_arrive_expect_tx(&full[s], (uint32_t)G::BYTES);
           unsigned char* st = smem + s * G::BYTES;
           const int cx = a.tx0 + lo - 2 - A + k * NC;
@@ -250,156 +245,235 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
         }
       }
     }
+    return;
+  }
+  // ------------------------------ consumers ------------------------------
+  const int t = tid;
+  const bool active = t < nvalid;
+  March<T, S, LIM, LIT, D> mr;
+  mr.smax = T(0);
+  mr.fin = 0xffffffffu;
+  mr.bad = false;
+  const T* pin;
+  T* pout;
+  if (CONTIG) {
+    const int64_t off = (pb + (active ? t : 0)) * a.t1stride + (int64_t)blockIdx.z * a.t2stride;
+    pin = a.qin + off;
+    pout = a.qout + off;
   } else {
-    // ------------------------------ consumers ------------------------------
-    const int t = tid;
-    const bool active = t < nvalid;
-    March<T, S, LIM, LIT> mr;
-    mr.smax = T(0);
-    mr.fin = 0xffffffffu;
-    const T* pin;
-    T* pout;
-    if (CONTIG) {
-      const int64_t off = (pb + (active ? t : 0)) * a.t1stride + (int64_t)blockIdx.z * a.t2stride;
-      pin = a.qin + off;
-      pout = a.qout + off;
-    } else {
-      const int64_t off = pb + (active ? t : 0) + (int64_t)blockIdx.z * a.t2stride;
-      pin = a.qin + off;
-      pout = a.qout + off;
-    }
-    const bool halo_lo = a.bc_lo == BC_HALO, halo_hi = a.bc_hi == BC_HALO;
-    const bool refl_lo = a.bc_lo == BC_REFLECTIVE, refl_hi = a.bc_hi == BC_REFLECTIVE;
-    unsigned char* outs = smem + NSTAGE * G::BYTES;  // contig output tiles
+    const int64_t off = pb + (active ? t : 0) + (int64_t)blockIdx.z * a.t2stride;
+    pin = a.qin + off;
+    pout = a.qout + off;
+  }
+  const bool halo_lo = a.bc_lo == BC_HALO, halo_hi = a.bc_hi == BC_HALO;
+  const bool refl_lo = a.bc_lo == BC_REFLECTIVE, refl_hi = a.bc_hi == BC_REFLECTIVE;
+  unsigned char* outs = smem + NSTAGE * G::BYTES;  // contig output tiles
 
-    auto fetch = [&](const unsigned char* st, int r, int c, T (&q)[M]) {
-      const int j = lo - 2 - A + r;
-      if (!CONTIG) {
-#pragma unroll
-        for (int k = 0; k < M; ++k)
-          q[k] = reinterpret_cast<const T*>(st)[(k * NC + c) * kConsumers + t];
-        const bool neg = (j < 0 && refl_lo) || (j >= a.n && refl_hi);
-        if (neg) {
-#pragma unroll
-          for (int k = 0; k < M; ++k)
-            if (k == a.nv) q[k] = -q[k];
-        }
-      } else {
+  // Ghost cells (boundary.py:87-122) are fixed up in the stage itself, once
+  // per stage that holds any, by the thread owning the row/column, so the
+  // per-cell fetch below is a plain branch-free shared-memory read:
+  //   contig: the TMA box read the memory ghosts; physical sides overwrite
+  //           them with the remapped interior value (negated for reflective);
+  //   strided: the producer already copied the remapped rows; reflective
+  //           sides negate the normal-velocity state.
+  // The generic-proxy writes are fenced before the stage goes back to the
+  // async proxy (the producer's next bulk copy into it).
+  auto patch = [&](unsigned char* st, int k) {
+    const int r0 = k * NC;
+    const int jlo = lo - 2 - A + r0;
+    if (CONTIG) {
+      const bool any = (jlo < 0 && !halo_lo) || (jlo + NC > a.n && !halo_hi);
+      if (!any) return;
+#pragma unroll 1
+      for (int c = 0; c < NC; ++c) {
+        const int j = jlo + c;
         const bool ghost = (j < 0 && !halo_lo) || (j >= a.n && !halo_hi);
-        if (!ghost) {
-#pragma unroll
-          for (int k = 0; k < M; ++k)
-            q[k] = *reinterpret_cast<const T*>(st + (k * kConsumers + t) * kRowStrideContig +
-                                               c * (int)sizeof(T));
-        } else {
-          bool neg;
-          const int js = remap(j, a.n, a.bc_lo, a.bc_hi, neg);
-#pragma unroll
-          for (int k = 0; k < M; ++k) q[k] = pin[js + k * a.sstride];
-          if (neg) {
-#pragma unroll
-            for (int k = 0; k < M; ++k)
-              if (k == a.nv) q[k] = -q[k];
-          }
-        }
-      }
-    };
-    // emit the updated cell e = r - A - 4 of the segment (cell lo + e).  Contig
-    // sweeps stage it in output tile e / NC (double-buffered) for a TMA store.
-    auto emit = [&](int k, int r, int c, bool valid, const T (&o)[M]) {
-      (void)k;
-      (void)c;
-      if (CONTIG) {
-        const int e = r - A - 4;
-        unsigned char* ob = outs + ((e / NC) & 1) * G::BYTES;
-#pragma unroll
-        for (int q = 0; q < M; ++q)
-          *reinterpret_cast<T*>(ob + (q * kConsumers + t) * kRowStrideContig +
-                                (e % NC) * (int)sizeof(T)) = o[q];
-        if (valid && active) {
-#pragma unroll
-          for (int q = 0; q < M; ++q) mr.fin = min(mr.fin, finite_key(o[q]));
-        }
-      } else if (valid && active) {
-        T* dst = pout + (int64_t)(lo + r - A - 4) * a.astride;
+        if (!ghost || r0 + c < A) continue;
+        bool neg;
+        const int js = remap(j, a.n, a.bc_lo, a.bc_hi, neg);
 #pragma unroll
         for (int q = 0; q < M; ++q) {
-          dst[q * a.sstride] = o[q];
-          mr.fin = min(mr.fin, finite_key(o[q]));
+          T v = pin[js + q * a.sstride];
+          if (neg && q == a.nv) v = -v;
+          *reinterpret_cast<T*>(st + (q * kConsumers + t) * kRowStrideContig + c * (int)sizeof(T)) = v;
         }
       }
-    };
-
-    // output tile `tile` complete in smem -> one TMA tensor store per state.
-    // Before the barrier, thread 0 makes sure the store of tile-2 (issued at
-    // the previous flush or earlier) has finished reading the buffer tile+1
-    // is about to be written into.
-    int flushed = -1;
-    auto flush = [&](int tile) {
-      fence_proxy_async_smem();
-      if (t == 0) bulk_wait_read<0>();
-      named_barrier_sync(1, kConsumers);
-      if (t == 0) {
-        const unsigned char* ob = outs + (tile & 1) * G::BYTES;
-        const int cx = a.tx0 + lo + tile * NC;
-        const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
-#pragma unroll
-        for (int q = 0; q < M; ++q)
-          tma_store_4d(maps.st, ob + q * kConsumers * kRowStrideContig, cx, cy, cz, q);
-        bulk_commit();
-      }
-      flushed = tile;
-    };
-
-    for (int k = 0; k < nst; ++k) {
-      const int s = k % NSTAGE;
-      mbar_wait(&full[s], (k / NSTAGE) & 1);
-      const unsigned char* st = smem + s * G::BYTES;
+    } else {
+      const bool any = (jlo < 0 && refl_lo) || (jlo + NC > a.n && refl_hi);
+      if (!any || a.nv < 0 || a.nv >= M) return;
 #pragma unroll 1
-      for (int g = 0; g < NC / 3; ++g) {
-        const int r0 = k * NC + 3 * g;
-        if (r0 >= ncell) break;
-        const int c0 = 3 * g;
-        T q[M];
-        if (r0 >= A + 4) {
-          T o[M];
-          bool v;
-          v = r0 < ncell;
-          fetch(st, r0, c0, q);
-          mr.template step<0>(q, a, v && active, o);
-          emit(k, r0, c0, v, o);
-          v = r0 + 1 < ncell;
-          fetch(st, r0 + 1, c0 + 1, q);
-          mr.template step<1>(q, a, v && active, o);
-          emit(k, r0 + 1, c0 + 1, v, o);
-          v = r0 + 2 < ncell;
-          fetch(st, r0 + 2, c0 + 2, q);
-          mr.template step<2>(q, a, v && active, o);
-          emit(k, r0 + 2, c0 + 2, v, o);
-          // the group's last cell closes an output tile every NC cells
-          if (CONTIG && (r0 + 2 - A - 4) % NC == NC - 1) flush((r0 + 2 - A - 4) / NC);
-        } else if (r0 == A + 1) {
-          fetch(st, r0, c0, q);
-          mr.template fan<0>(q, a, active);          // F(lo-1)
-          fetch(st, r0 + 1, c0 + 1, q);
-          mr.template fan<1>(q, a, active);          // F(lo)
-          fetch(st, r0 + 2, c0 + 2, q);
-          mr.template fan_corr<2>(q, a, active);     // F(lo+1), G(lo)
-        } else if (r0 == A - 2) {
-          fetch(st, r0 + 2, c0 + 2, q);
-          mr.template first<2>(q);                   // cell lo-2
-        }
+      for (int c = 0; c < NC; ++c) {
+        const int j = jlo + c;
+        if (!((j < 0 && refl_lo) || (j >= a.n && refl_hi)) || r0 + c < A) continue;
+        T* e = reinterpret_cast<T*>(st) + (a.nv * NC + c) * kConsumers + t;
+        *e = -*e;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
     }
+    fence_proxy_async_smem();
+  };
+  auto fetch = [&](const unsigned char* st, int c, T (&q)[M]) {
+    if (!CONTIG) {
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        q[k] = reinterpret_cast<const T*>(st)[(k * NC + c) * kConsumers + t];
+    } else {
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        q[k] = *reinterpret_cast<const T*>(st + (k * kConsumers + t) * kRowStrideContig +
+                                           c * (int)sizeof(T));
+    }
+  };
+  // emit the updated cell e = r - A - 4 of the segment (cell lo + e).  Contig
+  // sweeps stage it in output tile e / NC (double-buffered) for a TMA store.
+  auto emit = [&](int r, bool valid, const T (&o)[M]) {
     if (CONTIG) {
-      const int last = (ncell - 1 - A - 4) / NC;  // tile of the segment's last cell
-      if (last > flushed) flush(last);
-      if (t == 0) bulk_wait<0>();
+      const int e = r - A - 4;
+      unsigned char* ob = outs + ((e / NC) & 1) * G::BYTES;
+#pragma unroll
+      for (int q = 0; q < M; ++q)
+        *reinterpret_cast<T*>(ob + (q * kConsumers + t) * kRowStrideContig +
+                              (e % NC) * (int)sizeof(T)) = o[q];
+      if (valid && active) {
+#pragma unroll
+        for (int q = 0; q < M; ++q) mr.fin = min(mr.fin, finite_key(o[q]));
+      }
+    } else if (valid && active) {
+      T* dst = pout + (int64_t)(lo + r - A - 4) * a.astride;
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        dst[q * a.sstride] = o[q];
+        mr.fin = min(mr.fin, finite_key(o[q]));
+      }
     }
-    smax = mr.smax;
-    fin = mr.fin;
+  };
+
+  // output tile `tile` complete in smem -> one TMA tensor store per state.
+  // Before the barrier, thread 0 makes sure the store of tile-2 (issued at
+  // the previous flush or earlier) has finished reading the buffer tile+1
+  // is about to be written into.
+  int flushed = -1;
+  auto flush = [&](int tile) {
+    fence_proxy_async_smem();
+    if (t == 0) bulk_wait_read<0>();
+    named_barrier_sync(1, kConsumers);
+    if (t == 0) {
+      const unsigned char* ob = outs + (tile & 1) * G::BYTES;
+      const int cx = a.tx0 + lo + tile * NC;
+      const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
+#pragma unroll
+      for (int q = 0; q < M; ++q)
+        tma_store_4d(maps.st, ob + q * kConsumers * kRowStrideContig, cx, cy, cz, q);
+      bulk_commit();
+    }
+    flushed = tile;
+  };
+
+  for (int k = 0; k < nst; ++k) {
+    const int kk = k0 + k;
+    const int s = kk % NSTAGE;
+    mbar_wait(&full[s], (kk / NSTAGE) & 1);
+    unsigned char* st = smem + s * G::BYTES;
+    patch(st, k);
+#pragma unroll 1
+    for (int g = 0; g < NC / 3; ++g) {
+      const int r0 = k * NC + 3 * g;
+      if (r0 >= ncell) break;
+      const int c0 = 3 * g;
+      T q[M];
+      if (r0 >= A + 4) {
+        T o[M];
+        bool v;
+        v = r0 < ncell;
+        fetch(st, c0, q);
+        mr.template step<0>(q, a, v && active, o);
+        emit(r0, v, o);
+        v = r0 + 1 < ncell;
+        fetch(st, c0 + 1, q);
+        mr.template step<1>(q, a, v && active, o);
+        emit(r0 + 1, v, o);
+        v = r0 + 2 < ncell;
+        fetch(st, c0 + 2, q);
+        mr.template step<2>(q, a, v && active, o);
+        emit(r0 + 2, v, o);
+        // the group's last cell closes an output tile every NC cells
+        if (CONTIG && (r0 + 2 - A - 4) % NC == NC - 1) flush((r0 + 2 - A - 4) / NC);
+      } else if (r0 == A + 1) {
+        fetch(st, c0, q);
+        mr.template fan<0>(q, a, active);          // F(lo-1)
+        fetch(st, c0 + 1, q);
+        mr.template fan<1>(q, a, active);          // F(lo)
+        fetch(st, c0 + 2, q);
+        mr.template fan_corr<2>(q, a, active);     // F(lo+1), G(lo)
+      } else if (r0 == A - 2) {
+        fetch(st, c0 + 2, q);
+        mr.template first<2>(q);                   // cell lo-2
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (CONTIG) {
+    const int last = (ncell - 1 - A - 4) / NC;  // tile of the segment's last cell
+    if (last > flushed) flush(last);
+    if (t == 0) bulk_wait<0>();
+  }
+  smax = mr.smax;
+  fin = mr.fin;
+  bad = mr.bad && active;
+}
+
+// Number of stages one segment pass streams (same formula as segment_pass).
+template <typename T, class S, bool CONTIG>
+__device__ __forceinline__ int segment_stages(const SweepArgs<T>& a) {
+  using G = StageGeom<T, S, CONTIG>;
+  const int lo = blockIdx.y * a.seg_len;
+  const int hi = min(a.n, lo + a.seg_len);
+  return (hi - lo + G::A + 4 + G::NC - 1) / G::NC;
+}
+
+// ---------------------------------------------------------------------------
+// The sweep kernel.  Relative cell index r = 0 .. L+A+3 of a segment [lo, hi)
+// maps to pencil cell j = lo - 2 - A + r: r < A are alignment dummies, r =
+// A..A+3 the prologue (cells lo-2 .. lo+1), r >= A+4 emits cell lo + r - A - 4.
+//
+// Pass 1 marches with FastArith (branch-free IEEE division / square root).
+// If any consumer left the fast-path domain (zero/NaN depths, denormal-scale
+// data, overflow), the whole CTA runs pass 2 over the same segment with
+// ExactArith: it rewrites every output of the segment (same threads, or the
+// same TMA-issuing thread after bulk_wait), and its (smax, fin) replace pass
+// 1's.  Literal (blow-up) kernels run one ExactArith pass.
+template <typename T, class S, int LIM, bool LIT, bool CONTIG>
+__global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
+    sweep_kernel(const SweepArgs<T> a, const __grid_constant__ TmaMaps maps) {
+  using G = StageGeom<T, S, CONTIG>;
+  constexpr int NSTAGE = G::NSTAGE;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (NSTAGE + G::NOUT) * G::BYTES);
+  uint64_t* empty = full + NSTAGE;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  T smax = T(0);
+  uint32_t fin = 0xffffffffu;
+  bool bad = false;
+  if (LIT) {
+    segment_pass<T, S, LIM, LIT, CONTIG, ExactArith>(a, maps, smem, full, empty, 0, smax, fin, bad);
+  } else {
+    segment_pass<T, S, LIM, LIT, CONTIG, FastArith>(a, maps, smem, full, empty, 0, smax, fin, bad);
+    if (__syncthreads_or(bad)) {
+      smax = T(0);
+      fin = 0xffffffffu;
+      const int k0 = segment_stages<T, S, CONTIG>(a);
+      segment_pass<T, S, LIM, LIT, CONTIG, ExactArith>(a, maps, smem, full, empty, k0, smax, fin,
+                                                       bad);
+    }
   }
   finish_block<T>(smax, fin, a);
 }
@@ -468,7 +542,8 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
       const int x = b + lane;
       T q[M];
       load_cell<T, M>(qrow, a.sstride, 1, min(x, hi + 1), a, q);
-      Cell c = S::make(q);
+      bool bad_ = false;
+      Cell c = S::template make<ExactArith>(q, bad_);
 
       // left neighbour cell (x-1)
       Cell cl = c;
@@ -477,7 +552,7 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
         int i = 0;
         S::for_cell_regs(cl, [&](T& r) { r = carry[wib][1][i++]; });
       }
-      Fan F = S::solve(cl, c, a.P);
+      Fan F = S::template solve<ExactArith>(cl, c, a.P, bad_);
       if (x >= lo - 1 && x <= hi + 1) fold_speed<S, T>(F, a.P, smax);
 
       Fan F1 = F, F2 = F;
@@ -492,7 +567,7 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
         S::for_regs(F2, [&](T& r) { r = carry[wib][lane][i++]; });
       }
       T G[M];
-      correction<S, LIT, T>(F2, F1, F, a.P, a.dtdx, lim_id, G);
+      correction<S, LIT, ExactArith, T>(F2, F1, F, a.P, a.dtdx, lim_id, G, bad_);
       T G1[M], q2[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) {
@@ -542,8 +617,9 @@ __global__ void solve_pairs(const T* ql, const T* qr, T* W, T* s, int64_t n, Par
   T a[M], b[M];
 #pragma unroll
   for (int k = 0; k < M; ++k) { a[k] = ql[i * M + k]; b[k] = qr[i * M + k]; }
-  typename S::Cell L = S::make(a), R = S::make(b);
-  typename S::Fan f = S::solve(L, R, P);
+  bool bad = false;
+  typename S::Cell L = S::template make<ExactArith>(a, bad), R = S::template make<ExactArith>(b, bad);
+  typename S::Fan f = S::template solve<ExactArith>(L, R, P, bad);
 #pragma unroll
   for (int p = 0; p < S::NW; ++p) {
     s[i * S::NW + p] = S::speed(f, P, p);
