@@ -16,6 +16,9 @@
  *   clb_attempt_step           the sweep loop of Simulation.attempt_step
  *                              (timestep.py:195-211); the fp64 accept/revert
  *                              arithmetic stays on the host (timestep.py:212-239)
+ *   clb_run_batch              Simulation.run_until's attempt loop  timestep.py:245-285
+ *                              with estimate_dt / attempt_step      timestep.py:151-243
+ *                              evaluated on the device (fp64, same expressions)
  *   clb_first_nonfinite        Simulation._check_finite             timestep.py:179-186
  *   clb_solve_pairs            RiemannSolver.solve                  riemann.py:205-223
  *   clb_last_error             (exceptions never cross the ABI)
@@ -157,6 +160,47 @@ int clb_halo_copy(clb_handle h, int buf, int side, int to_host, void *host);
  * W out (n, nw, m), s out (n, nw). */
 int clb_solve_pairs(clb_handle h, int axis, int64_t n, const void *ql, const void *qr,
                     void *W, void *s);
+
+/* Device-resident run loop (timestep.py:245-285 run_until between two stop
+ * times).  Attempts run back to back from a CUDA graph: the ndim sweeps read
+ * their buffers and dt from a device control block, and a one-thread
+ * controller kernel evaluates each attempt with the reference's fp64
+ * expressions (timestep.py:151-243: dt = (cfl_target*min_dx)/s capped and
+ * clipped to `stop`, nu = (dt*s)/min_dx, accept iff nu <= cfl_max, buffer
+ * rotation, t = stop if landed else t + dt, dt_retry, the two-revert
+ * instability check) and prepares the next one, so the dt sequence is
+ * bit-identical to the host loop.  The batch ends when t reaches `stop`,
+ * `max_accepted` attempts were accepted (< 0: no limit), the attempt log is
+ * full, or an attempt fails; one device->host read at the end.
+ * In: every field up to and including max_accepted.  Out: the controller
+ * fields (t .. scratch1) and n_attempts .. fail_dt. */
+#define CLB_BATCH_STOP 0      /* t reached stop                                  */
+#define CLB_BATCH_MAXSTEPS 1  /* max_accepted attempts accepted                   */
+#define CLB_BATCH_LOGFULL 2   /* log_cap attempts recorded; call again            */
+#define CLB_BATCH_BLOWUP 3    /* attempt n_attempts produced a non-finite value in
+                                 sweep fail_sweep (not logged; buffers untouched)  */
+#define CLB_BATCH_UNSTABLE 4  /* the last logged attempt was a second consecutive
+                                 revert without improvement (UnstableStepError)   */
+#define CLB_BATCH_DTERR 5     /* no finite dt (no wave speed, no cap, no stop)   */
+
+typedef struct clb_batch {
+    double t, last_max_speed, prev_nu, nu_max;
+    int32_t prev_reverted;
+    int32_t cur, scratch0, scratch1;   /* buffer roles (timestep.py:113,216-219) */
+    double stop, cfl_target, cfl_max, dt_cap, min_spacing;
+    int64_t max_accepted;
+    int64_t n_attempts, n_accepted;
+    int32_t status, fail_sweep;
+    double fail_dt;
+} clb_batch;
+
+/* One logged attempt (timestep.py:45-55 StepAttempt). */
+typedef struct clb_attempt {
+    double t_start, dt, max_speed, nu, dt_retry;
+    int32_t accepted, landed;
+} clb_attempt;
+
+int clb_run_batch(clb_handle h, clb_batch *b, clb_attempt *log, int64_t log_cap);
 
 /* Self-test of the branch-free fp64 division / square root used by the
  * sweep kernels (clb_solvers.cuh FastArith) against div.rn.f64 /

@@ -34,8 +34,11 @@ EXPORTS = (
     "clb_download_padded", "clb_set_boundary", "clb_sweep", "clb_sweep_async", "clb_fetch",
     "clb_attempt_step", "clb_first_nonfinite", "clb_halo_layout", "clb_halo_copy", "clb_solve_pairs",
     "clb_enable_timing", "clb_timing", "clb_host_alloc", "clb_host_free", "clb_memory_info",
-    "clb_selftest_arith",
+    "clb_selftest_arith", "clb_run_batch",
 )
+
+#: clb_run_batch statuses (include/clawb200.h)
+BATCH_STOP, BATCH_MAXSTEPS, BATCH_LOGFULL, BATCH_BLOWUP, BATCH_UNSTABLE, BATCH_DTERR = range(6)
 
 
 class ClbDesc(ctypes.Structure):
@@ -51,6 +54,29 @@ class ClbDesc(ctypes.Structure):
         ("params", ctypes.c_double * 8),
         ("bc", (ctypes.c_int32 * 2) * 3),
         ("normal_velocity", ctypes.c_int32 * 3),
+    ]
+
+
+class ClbBatch(ctypes.Structure):
+    _fields_ = [
+        ("t", ctypes.c_double), ("last_max_speed", ctypes.c_double),
+        ("prev_nu", ctypes.c_double), ("nu_max", ctypes.c_double),
+        ("prev_reverted", ctypes.c_int32),
+        ("cur", ctypes.c_int32), ("scratch0", ctypes.c_int32), ("scratch1", ctypes.c_int32),
+        ("stop", ctypes.c_double), ("cfl_target", ctypes.c_double), ("cfl_max", ctypes.c_double),
+        ("dt_cap", ctypes.c_double), ("min_spacing", ctypes.c_double),
+        ("max_accepted", ctypes.c_int64),
+        ("n_attempts", ctypes.c_int64), ("n_accepted", ctypes.c_int64),
+        ("status", ctypes.c_int32), ("fail_sweep", ctypes.c_int32),
+        ("fail_dt", ctypes.c_double),
+    ]
+
+
+class ClbAttempt(ctypes.Structure):
+    _fields_ = [
+        ("t_start", ctypes.c_double), ("dt", ctypes.c_double), ("max_speed", ctypes.c_double),
+        ("nu", ctypes.c_double), ("dt_retry", ctypes.c_double),
+        ("accepted", ctypes.c_int32), ("landed", ctypes.c_int32),
     ]
 
 
@@ -104,6 +130,7 @@ def lib():
         "clb_host_free": (None, [_vp]),
         "clb_memory_info": (_int, [_vp, ctypes.POINTER(_sz), ctypes.POINTER(_i64)]),
         "clb_selftest_arith": (_int, [_int, _i64, _vp, _vp, ctypes.POINTER(_i64)]),
+        "clb_run_batch": (_int, [_vp, ctypes.POINTER(ClbBatch), ctypes.POINTER(ClbAttempt), _i64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -280,6 +307,13 @@ class DeviceGrid:
         _check(lib().clb_solve_pairs(self.handle, axis, n, ql.ctypes.data, qr.ctypes.data,
                                      W.ctypes.data, s.ctypes.data), self.handle)
         return W, s
+
+    def run_batch(self, batch: "ClbBatch", log_cap: int = 4096):
+        """Device-resident attempt loop (clb_run_batch): updates `batch` in
+        place and returns the logged attempts."""
+        log = (ClbAttempt * log_cap)()
+        _check(lib().clb_run_batch(self.handle, ctypes.byref(batch), log, log_cap), self.handle)
+        return [log[i] for i in range(batch.n_attempts)]
 
     def enable_timing(self, on: bool = True):
         _check(lib().clb_enable_timing(self.handle, 1 if on else 0), self.handle)

@@ -57,7 +57,14 @@ struct clb_ctx {
   Result* h_res = nullptr;
   int num_sms = 148;
   int seg_override[3] = {0, 0, 0};
-  clb::TmaMaps maps[3][3];  // [src][dst]: load map of src, store map of dst
+  clb::TmaMaps maps;        // per buffer: load map, store map
+  // device-resident controller (clb_run_batch)
+  clb::DevCtl* d_ctl = nullptr;
+  clb::DevCtl* h_ctl = nullptr;
+  clb_attempt* d_log = nullptr;
+  int64_t log_cap = 0;
+  cudaGraphExec_t batch_exec = nullptr;
+  cudaGraph_t batch_graph = nullptr;
   bool have_maps = false;
   bool timing = false;
   std::vector<TimedLaunch> launches;
@@ -155,6 +162,11 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   const int64_t isz = h->itemsize;
   g.qin = (const char*)h->buf[src] + h->origin * isz;
   g.qout = (char*)h->buf[dst] + h->origin * isz;
+  g.src = src;
+  g.dst = dst;
+  g.axis = axis;
+  g.spacing = h->d.spacing[axis];
+  for (int b = 0; b < 3; ++b) g.bufs[b] = (const char*)h->buf[b] + h->origin * isz;
   g.sstride = h->sstride;
   g.bc_lo = h->d.bc[axis][0];
   g.bc_hi = h->d.bc[axis][1];
@@ -180,7 +192,7 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
     g.contig = (contig_mode == 2 && h->have_maps) ? 2 : 1;
     g.n = (int)nx; g.n1 = (int)ny; g.n2 = (int)nz;
     g.astride = 1; g.t1stride = h->ystride; g.t2stride = h->zstride;
-    g.maps = &h->maps[src][dst];
+    g.maps = &h->maps;
     g.tx0 = (int)h->xoff;
     g.ty0 = h->ndim >= 2 ? 2 : 0;
     g.tz0 = h->ndim == 3 ? 2 : 0;
@@ -201,7 +213,11 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   // contig stages are 48 bytes of a row: segment starts must stay aligned
   const int64_t align = (axis == 0 && g.contig == 2) ? 48 / h->itemsize : 1;
   int64_t nseg = (target_ctas + pen_ctas - 1) / pen_ctas;
-  nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, g.n / 32));
+  static const int64_t min_seg = [] {
+    const char* e = getenv("CLB_MIN_SEG");
+    return e ? std::max<int64_t>(4, atoll(e)) : (int64_t)32;
+  }();
+  nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, g.n / min_seg));
   int64_t L = (g.n + nseg - 1) / nseg;
   if (h->seg_override[axis] > 0) L = h->seg_override[axis];
   L = (L + align - 1) / align * align;
@@ -210,13 +226,16 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   return g;
 }
 
-int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bool literal) {
+// indirect: buffers and dt are read by the kernel from h->d_ctl (batch graphs)
+int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bool literal,
+                 bool indirect = false) {
   if (axis < 0 || axis >= h->ndim) return fail(h, CLB_EINVAL, "sweep axis out of range");
   if (src < 0 || src > 2 || dst < 0 || dst > 2) return fail(h, CLB_EINVAL, "buffer index out of range");
   if (src == dst) return fail(h, CLB_EINVAL, "sweep cannot run in place");
   if (!(dt > 0.0)) return fail(h, CLB_EINVAL, "dt must be positive");
   if (slot < 0 || slot > 3) return fail(h, CLB_EINVAL, "result slot out of range");
   clb::GenericArgs g = sweep_geometry(h, axis, src, dst);
+  g.ctl = indirect ? h->d_ctl : nullptr;
   // sweep.py:336-337: dtdx = T(dt / dx[axis]) -- fp64 divide, then round to T.
   const double dtdx64 = dt / h->d.spacing[axis];
   g.dtdx = h->itemsize == 8 ? dtdx64 : (double)(float)dtdx64;
@@ -224,7 +243,7 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
   g.smax_bits = &h->d_res->smax[slot];
   g.nonfinite = &h->d_res->nonfinite[slot];
   TimedLaunch tl{axis, nullptr, nullptr};
-  if (h->timing) {
+  if (h->timing && !indirect) {
     tl.a = take_event(h);
     tl.b = take_event(h);
     cudaEventRecord(tl.a, h->stream);
@@ -252,7 +271,7 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
       break;
   }
   if (e != cudaSuccess) return cuda_fail(h, e, "sweep launch");
-  if (h->timing) {
+  if (h->timing && !indirect) {
     cudaEventRecord(tl.b, h->stream);
     h->launches.push_back(tl);
   }
@@ -318,6 +337,108 @@ __global__ void selftest_arith_kernel(const double* a, const double* b, int64_t 
   if (!cs && __float_as_int(sff) != __float_as_int(__fsqrt_rn(xf))) atomicAdd(&cnt[5], 1ull);
   if (cq) atomicAdd(&cnt[6], 1ull);
   if (cs) atomicAdd(&cnt[7], 1ull);
+}
+
+
+// ---------------------------------------------------------------------------
+// Device-resident controller (clb_run_batch): timestep.py:151-243 in fp64 on
+// one device thread.  Every expression keeps the reference's operation order
+// (explicit __d*_rn so nothing is contracted); Python's min(a, b) / max(a, b)
+// are "b if b < a else a" / "b if b > a else a".
+
+// estimate_dt (timestep.py:151-177) + the run_until loop guards
+// (timestep.py:263-270) for the next attempt, or end the batch.
+__device__ void ctl_prepare_next(clb::DevCtl* c) {
+  if (c->done) return;
+  if (c->max_accepted >= 0 && c->n_accepted >= c->max_accepted) {
+    c->status = CLB_BATCH_MAXSTEPS; c->done = 1; return;
+  }
+  if (!(c->t < c->stop)) { c->status = CLB_BATCH_STOP; c->done = 1; return; }
+  if (c->n_attempts >= c->log_cap) { c->status = CLB_BATCH_LOGFULL; c->done = 1; return; }
+  const double s = c->last_max_speed;
+  double dt;
+  if (s > 0.0) {
+    dt = __ddiv_rn(__dmul_rn(c->cfl_target, c->min_spacing), s);
+    dt = c->dt_cap < dt ? c->dt_cap : dt;
+  } else {
+    dt = c->dt_cap;
+  }
+  int landed = 0;
+  const double remaining = __dsub_rn(c->stop, c->t);
+  if (dt >= remaining) {
+    dt = remaining;
+    landed = 1;
+  }
+  if (!isfinite(dt)) { c->status = CLB_BATCH_DTERR; c->done = 1; return; }
+  c->dt = dt;
+  c->landed = landed;
+  // timestep.py:200-206: sweep j reads the previous output, writes scratch[j % 2]
+  int cur = c->cur;
+  for (int j = 0; j < c->ndim; ++j) {
+    const int dst = (j % 2 == 0) ? c->s0 : c->s1;
+    c->src[j] = cur;
+    c->dst[j] = dst;
+    cur = dst;
+  }
+}
+
+__global__ void ctl_prepare(clb::DevCtl* c) { ctl_prepare_next(c); }
+
+// The attempt's verdict (timestep.py:207-243), then the next attempt.
+__global__ void ctl_finish(clb::DevCtl* c, Result* r) {
+  if (c->done) return;
+  double step_speed = 0.0;
+  for (int j = 0; j < c->ndim; ++j) {
+    if (r->nonfinite[j]) {
+      c->status = CLB_BATCH_BLOWUP;
+      c->fail_sweep = j;
+      c->done = 1;
+      return;
+    }
+    const double sj = __longlong_as_double((long long)r->smax[j]);
+    step_speed = sj > step_speed ? sj : step_speed;
+  }
+  for (int j = 0; j < 4; ++j) { r->smax[j] = 0ull; r->nonfinite[j] = 0; }
+  const double nu = __ddiv_rn(__dmul_rn(c->dt, step_speed), c->min_spacing);
+  const bool accepted = nu <= c->cfl_max;
+  clb_attempt rec;
+  rec.t_start = c->t;
+  rec.dt = c->dt;
+  rec.max_speed = step_speed;
+  rec.nu = nu;
+  rec.dt_retry = __longlong_as_double(0x7ff8000000000000ll);  // None
+  rec.accepted = accepted ? 1 : 0;
+  rec.landed = (c->landed && accepted) ? 1 : 0;
+  clb_attempt* log = (clb_attempt*)c->log;
+  if (accepted) {
+    const int last = (c->ndim - 1) % 2;
+    const int fin = last == 0 ? c->s0 : c->s1;
+    const int other = last == 0 ? c->s1 : c->s0;
+    c->s0 = c->cur;
+    c->s1 = other;
+    c->cur = fin;
+    c->t = c->landed ? c->stop : __dadd_rn(c->t, c->dt);
+    c->n_accepted += 1;
+    c->nu_max = nu > c->nu_max ? nu : c->nu_max;
+    c->prev_reverted = 0;
+  } else {
+    rec.dt_retry = __ddiv_rn(__dmul_rn(c->cfl_target, c->min_spacing), step_speed);
+    if (c->prev_reverted && nu >= c->prev_nu) {
+      // UnstableStepError: logged (the reference counts the revert first),
+      // prev_nu kept for the message, last_max_speed not updated
+      log[c->n_attempts] = rec;
+      c->n_attempts += 1;
+      c->status = CLB_BATCH_UNSTABLE;
+      c->done = 1;
+      return;
+    }
+    c->prev_reverted = 1;
+    c->prev_nu = nu;
+  }
+  c->last_max_speed = step_speed;
+  log[c->n_attempts] = rec;
+  c->n_attempts += 1;
+  ctl_prepare_next(c);
 }
 
 extern "C" {
@@ -393,11 +514,9 @@ int clb_create(const clb_desc* desc, clb_handle* out) {
     cudaMemsetAsync(h->buf[i], 0, h->buf_bytes, h->stream);
   }
   h->have_maps = true;
-  for (int sb = 0; sb < 3 && h->have_maps; ++sb)
-    for (int db = 0; db < 3; ++db)
-      if (sb != db && !(make_tensor_map(h, sb, false, h->maps[sb][db].ld) &&
-                        make_tensor_map(h, db, true, h->maps[sb][db].st)))
-        h->have_maps = false;
+  for (int b = 0; b < 3 && h->have_maps; ++b)
+    if (!(make_tensor_map(h, b, false, h->maps.ld[b]) && make_tensor_map(h, b, true, h->maps.st[b])))
+      h->have_maps = false;
   e = cudaMalloc(&h->d_res, sizeof(Result));
   if (e == cudaSuccess) e = cudaMallocHost(&h->h_res, sizeof(Result));
   if (e == cudaSuccess) e = cudaMemsetAsync(h->d_res, 0, sizeof(Result), h->stream);
@@ -421,6 +540,11 @@ int clb_destroy(clb_handle h) {
     if (h->buf[i]) cudaFree(h->buf[i]);
   if (h->d_res) cudaFree(h->d_res);
   if (h->h_res) cudaFreeHost(h->h_res);
+  if (h->batch_exec) cudaGraphExecDestroy(h->batch_exec);
+  if (h->batch_graph) cudaGraphDestroy(h->batch_graph);
+  if (h->d_ctl) cudaFree(h->d_ctl);
+  if (h->h_ctl) cudaFreeHost(h->h_ctl);
+  if (h->d_log) cudaFree(h->d_log);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
   return CLB_OK;
@@ -435,6 +559,10 @@ int clb_set_stream(clb_handle h, void* s) {
 int clb_set_segments(clb_handle h, int axis, int seg_len) {
   if (!h || axis < 0 || axis > 2 || seg_len < 0) return fail(h, CLB_EINVAL, "bad segment override");
   h->seg_override[axis] = seg_len;
+  if (h->batch_exec) cudaGraphExecDestroy(h->batch_exec);
+  if (h->batch_graph) cudaGraphDestroy(h->batch_graph);
+  h->batch_exec = nullptr;
+  h->batch_graph = nullptr;
   return CLB_OK;
 }
 
@@ -715,6 +843,10 @@ extern "C" int clb_set_boundary(clb_handle h, int axis, int lo, int hi) {
     return fail(h, CLB_EINVAL, "periodic boundary must be set on both sides");
   h->d.bc[axis][0] = lo;
   h->d.bc[axis][1] = hi;
+  if (h->batch_exec) cudaGraphExecDestroy(h->batch_exec);
+  if (h->batch_graph) cudaGraphDestroy(h->batch_graph);
+  h->batch_exec = nullptr;
+  h->batch_graph = nullptr;
   return CLB_OK;
 }
 
@@ -733,5 +865,119 @@ extern "C" int clb_halo_copy(clb_handle h, int buf, int side, int to_host, void*
       CLB_CUDA(h, cudaMemcpyAsync((char*)recv + k * ss, hp, bb, cudaMemcpyHostToDevice, h->stream));
   }
   CLB_CUDA(h, cudaStreamSynchronize(h->stream));
+  return CLB_OK;
+}
+
+namespace {
+
+// One attempt as a graph: ndim indirect sweeps + the controller.
+int build_batch_graph(clb_ctx* h) {
+  // configure every kernel outside capture: no-op launches (done = 1)
+  h->h_ctl->done = 1;
+  CLB_CUDA(h, cudaMemcpyAsync(h->d_ctl, h->h_ctl, sizeof(clb::DevCtl), cudaMemcpyHostToDevice,
+                              h->stream));
+  for (int j = 0; j < h->ndim; ++j) {
+    const int r = launch_sweep(h, j, 1.0, 0, 1, j, false, true);
+    if (r) return r;
+  }
+  CLB_CUDA(h, cudaStreamSynchronize(h->stream));
+  CLB_CUDA(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  int r = 0;
+  for (int j = 0; j < h->ndim && !r; ++j) r = launch_sweep(h, j, 1.0, 0, 1, j, false, true);
+  if (!r) ctl_finish<<<1, 1, 0, h->stream>>>(h->d_ctl, h->d_res);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+  if (r) { if (g) cudaGraphDestroy(g); return r; }
+  if (e != cudaSuccess) return cuda_fail(h, e, "batch graph capture");
+  h->batch_graph = g;
+  CLB_CUDA(h, cudaGraphInstantiate(&h->batch_exec, g, 0));
+  return CLB_OK;
+}
+
+}  // namespace
+
+extern "C" int clb_run_batch(clb_handle h, clb_batch* b, clb_attempt* log, int64_t log_cap) {
+  if (!h || !b || (!log && log_cap > 0)) return fail(h, CLB_EINVAL, "null argument");
+  if (log_cap < 1) return fail(h, CLB_EINVAL, "log_cap must be positive");
+  const int roles[3] = {b->cur, b->scratch0, b->scratch1};
+  for (int i = 0; i < 3; ++i)
+    if (roles[i] < 0 || roles[i] > 2) return fail(h, CLB_EINVAL, "buffer index out of range");
+  if (b->cur == b->scratch0 || b->cur == b->scratch1 || b->scratch0 == b->scratch1)
+    return fail(h, CLB_EINVAL, "step buffers must be distinct");
+  CLB_CUDA(h, cudaSetDevice(h->d.device));
+  if (!h->d_ctl) {
+    CLB_CUDA(h, cudaMalloc(&h->d_ctl, sizeof(clb::DevCtl)));
+    CLB_CUDA(h, cudaMallocHost(&h->h_ctl, sizeof(clb::DevCtl)));
+  }
+  if (h->log_cap < log_cap) {
+    if (h->d_log) cudaFree(h->d_log);
+    h->d_log = nullptr;
+    h->log_cap = 0;
+    CLB_CUDA(h, cudaMalloc(&h->d_log, (size_t)log_cap * sizeof(clb_attempt)));
+    h->log_cap = log_cap;
+  }
+  if (!h->batch_exec) {
+    const int r = build_batch_graph(h);
+    if (r) return r;
+  }
+  clb::DevCtl& c = *h->h_ctl;
+  std::memset(&c, 0, sizeof(c));
+  c.t = b->t;
+  c.last_max_speed = b->last_max_speed;
+  c.prev_nu = b->prev_nu;
+  c.nu_max = b->nu_max;
+  c.prev_reverted = b->prev_reverted ? 1 : 0;
+  c.cur = b->cur;
+  c.s0 = b->scratch0;
+  c.s1 = b->scratch1;
+  c.stop = b->stop;
+  c.cfl_target = b->cfl_target;
+  c.cfl_max = b->cfl_max;
+  c.dt_cap = b->dt_cap;
+  c.min_spacing = b->min_spacing;
+  c.max_accepted = b->max_accepted;
+  c.log_cap = log_cap;
+  c.ndim = h->ndim;
+  c.status = -1;
+  c.fail_sweep = -1;
+  c.log = h->d_log;
+  CLB_CUDA(h, cudaMemcpyAsync(h->d_ctl, h->h_ctl, sizeof(clb::DevCtl), cudaMemcpyHostToDevice,
+                              h->stream));
+  CLB_CUDA(h, cudaMemsetAsync(h->d_res, 0, sizeof(Result), h->stream));
+  ctl_prepare<<<1, 1, 0, h->stream>>>(h->d_ctl);
+  CLB_CUDA(h, cudaGetLastError());
+  // Replay attempts in chunks; the host only polls the done flag between
+  // chunks (attempts replayed past the end are no-ops).  A step budget sizes
+  // the first chunk exactly.
+  static const int64_t chunk_cap = [] {
+    const char* e = getenv("CLB_BATCH_CHUNK");
+    return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)256;
+  }();
+  int64_t chunk = b->max_accepted >= 0 ? std::max<int64_t>(1, std::min<int64_t>(b->max_accepted, chunk_cap))
+                                       : std::min<int64_t>(8, chunk_cap);
+  for (;;) {
+    for (int64_t i = 0; i < chunk; ++i) CLB_CUDA(h, cudaGraphLaunch(h->batch_exec, h->stream));
+    CLB_CUDA(h, cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(clb::DevCtl), cudaMemcpyDeviceToHost,
+                                h->stream));
+    CLB_CUDA(h, cudaStreamSynchronize(h->stream));
+    if (c.done) break;
+    chunk = std::min<int64_t>(std::min<int64_t>(2 * chunk, 64), chunk_cap);
+  }
+  if (c.n_attempts > 0)
+    CLB_CUDA(h, cudaMemcpy(log, h->d_log, (size_t)c.n_attempts * sizeof(clb_attempt),
+                           cudaMemcpyDeviceToHost));
+  b->t = c.t;
+  b->last_max_speed = c.last_max_speed;
+  b->prev_nu = c.prev_nu;
+  b->nu_max = c.nu_max;
+  b->prev_reverted = c.prev_reverted;
+  b->cur = c.cur;
+  b->scratch0 = c.s0;
+  b->scratch1 = c.s1;
+  b->n_attempts = c.n_attempts;
+  b->n_accepted = c.n_accepted;
+  b->status = c.status;
+  b->fail_sweep = c.fail_sweep;
+  b->fail_dt = c.dt;
   return CLB_OK;
 }

@@ -41,6 +41,24 @@ constexpr int kConsumers = 128;        // pencils per CTA
 constexpr int kThreads = kConsumers + 32;
 constexpr int kRowStrideContig = 48;   // bytes per row per state in a contig stage
 
+// Device-resident step controller state (clb_capi.cu ctl_* kernels; the
+// fp64 controller of timestep.py:151-243 run on the device between the
+// sweeps of a batch).  Sweeps launched "indirectly" read their buffers and
+// dt from here, so a whole run can be replayed from a CUDA graph without a
+// host round trip per attempt.
+struct DevCtl {
+  double t, last_max_speed, prev_nu, nu_max;
+  double stop, cfl_target, cfl_max, dt_cap, min_spacing;
+  double dt;                 // current attempt
+  long long max_accepted;    // < 0: unlimited
+  long long n_attempts, n_accepted, log_cap;
+  int prev_reverted, landed;
+  int cur, s0, s1;
+  int src[3], dst[3];        // buffer roles of the current attempt's sweeps
+  int done, status, fail_sweep, ndim;
+  void* log;                 // clb_attempt[log_cap]
+};
+
 template <typename T> struct SweepArgs {
   const T* qin;     // element (0,0,0) of state 0 (interior origin)
   T* qout;
@@ -58,14 +76,67 @@ template <typename T> struct SweepArgs {
   unsigned long long* smax_bits;
   int* nonfinite;
   int tx0, ty0, tz0;  // tensor-map coordinates of interior cell (0,0,0)
+  int src, dst;       // buffer indices (select the TMA maps)
+  // indirect launch (ctl != nullptr): src, dst and dt come from the
+  // controller; bufs are the three buffers' interior origins
+  const DevCtl* ctl;
+  int axis;
+  double spacing;
+  const void* bufs[3];
 };
 
-// TMA descriptors of the source (load) and destination (store) buffers of a
-// contiguous-axis sweep, passed by value as a __grid_constant__ parameter.
+// TMA descriptors of the three buffers (load: full padded extent; store:
+// interior-clipped), passed by value as a __grid_constant__ parameter.
 struct TmaMaps {
-  alignas(64) unsigned char ld[128];
-  alignas(64) unsigned char st[128];
+  alignas(64) unsigned char ld[3][128];
+  alignas(64) unsigned char st[3][128];
 };
+
+// Per-launch values that an indirect launch reads from the controller:
+// buffers (and with them the TMA maps) and dtdx.  Kept out of SweepArgs so
+// the kernel never writes into a copy of its by-value parameter (nvcc 12.9
+// dropped such stores and kept reading the parameter's original fields).
+template <typename T> struct Live {
+  const T* qin;
+  T* qout;
+  T dtdx;
+  int src, dst;
+};
+
+// Returns false if the controller has finished (graph replays past the end
+// of a run are no-ops).
+template <typename T> __device__ __forceinline__ bool resolve_live(const SweepArgs<T>& a,
+                                                                   Live<T>& L) {
+  int src = a.src, dst = a.dst;
+  T dtdx = a.dtdx;
+  if (a.ctl != nullptr) {
+    const DevCtl* c = a.ctl;
+    if (c->done) return false;
+    src = c->src[a.axis];
+    dst = c->dst[a.axis];
+    // sweep.py:336-337: dtdx = T(dt / dx[axis]), IEEE fp64 division then rounding
+    dtdx = (T)(c->dt / a.spacing);
+  }
+  // Both launch kinds select the buffers from bufs[] by index.  (Assigning
+  // a.qin on the direct path and a selected buffer on the indirect one made
+  // nvcc 12.9 fold the pointer back to a.qin for both.)
+  L.src = src;
+  L.dst = dst;
+  L.dtdx = dtdx;
+  L.qin = (const T*)(src == 0 ? a.bufs[0] : (src == 1 ? a.bufs[1] : a.bufs[2]));
+  L.qout = (T*)const_cast<void*>(dst == 0 ? a.bufs[0] : (dst == 1 ? a.bufs[1] : a.bufs[2]));
+  return true;
+}
+
+// Conditional IEEE negation (boundary.py:114,122 `*= -1.0`) as a sign-bit
+// flip.  Written on the bit pattern so the compiler cannot turn the
+// "negate state nv" loop into a dynamically indexed local-memory array.
+__device__ __forceinline__ double neg_if(double v, bool f) {
+  return __hiloint2double(__double2hiint(v) ^ (f ? (int)0x80000000 : 0), __double2loint(v));
+}
+__device__ __forceinline__ float neg_if(float v, bool f) {
+  return __int_as_float(__float_as_int(v) ^ (f ? (int)0x80000000 : 0));
+}
 
 // boundary.py:108-122 as a read-side index map: ghost cell j of a pencil
 // reads interior cell remap(j), negating state nv for reflective walls.
@@ -113,6 +184,9 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
   }
 }
 
+#ifndef CLB_CONTIG_NSTAGE
+#define CLB_CONTIG_NSTAGE 3
+#endif
 #ifndef CLB_SW_MINB
 #define CLB_SW_MINB 2
 #endif
@@ -130,7 +204,7 @@ template <typename T, class S, bool CONTIG> struct StageGeom {
   // 3-cell group starts on ring phase 0, and every contig stage box starts
   // 16-byte aligned (TMA requirement) because segments start at multiples of NC.
   static constexpr int A = 2;
-  static constexpr int NSTAGE_RAW = CONTIG ? (S::M >= 4 ? 2 : 3) : (72 * 1024 / BYTES);
+  static constexpr int NSTAGE_RAW = CONTIG ? (S::M >= 4 ? 2 : CLB_CONTIG_NSTAGE) : (72 * 1024 / BYTES);
   static constexpr int NSTAGE = NSTAGE_RAW < 2 ? 2 : (NSTAGE_RAW > 6 ? 6 : NSTAGE_RAW);
   static constexpr int NOUT = CONTIG ? 2 : 0;  // output staging tiles (TMA store)
   static constexpr int SMEM = (NSTAGE + NOUT) * BYTES + 2 * NSTAGE * 8;
@@ -151,6 +225,7 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
   T smax;
   uint32_t fin;
   bool bad;
+  T dtdx;
 
   __device__ __forceinline__ int lim(const SweepArgs<T>& a) const { return LIM >= 0 ? LIM : a.lim_id; }
 
@@ -169,14 +244,14 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
                                                             const SweepArgs<T>& a, bool fold) {
     constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
     fan<P>(q, a, fold);
-    correction<S, LIT, D, T>(F[P2], F[P1], F[P], a.P, a.dtdx, lim(a), G[P1], bad);
+    correction<S, LIT, D, T>(F[P2], F[P1], F[P], a.P, dtdx, lim(a), G[P1], bad);
   }
   // steady step: returns the updated cell i-2 in `out`
   template <int P> __device__ __forceinline__ void step(const T (&q)[M], const SweepArgs<T>& a,
                                                         bool fold, T (&out)[M]) {
     constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
     fan_corr<P>(q, a, fold);
-    update<S, LIT, T>(X[P2].q, F[P2], F[P1], G[P1], G[P2], a.P, a.dtdx, out);
+    update<S, LIT, T>(X[P2].q, F[P2], F[P1], G[P1], G[P2], a.P, dtdx, out);
   }
 };
 
@@ -186,11 +261,14 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
 // running stage sequence (mbarrier phases continue across passes).  Returns
 // the consumer's (smax, fin, bad) in the references.
 template <typename T, class S, int LIM, bool LIT, bool CONTIG, class D>
-__device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const TmaMaps& maps,
+__device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T>& L,
+                                             const TmaMaps& maps_all,
                                              unsigned char* smem, uint64_t* full, uint64_t* empty,
                                              int k0, T& smax, uint32_t& fin, bool& bad) {
   using G = StageGeom<T, S, CONTIG>;
   constexpr int NC = G::NC, NSTAGE = G::NSTAGE, M = S::M, A = G::A;
+  const unsigned char* map_ld = maps_all.ld[L.src];
+  const unsigned char* map_st = maps_all.st[L.dst];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int seg = blockIdx.y;
@@ -210,7 +288,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const TmaMap
     if (lane == 0) {
       if (!CONTIG) {
         const uint32_t colbytes = (uint32_t)(((nvalid * isz) + 15) & ~15);
-        const T* base = a.qin + pb + (int64_t)blockIdx.z * a.t2stride;
+        const T* base = L.qin + pb + (int64_t)blockIdx.z * a.t2stride;
         for (int k = 0; k < nst; ++k) {
           const int kk = k0 + k;
           const int s = kk % NSTAGE;
@@ -241,7 +319,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const TmaMap
           const int cx = a.tx0 + lo - 2 - A + k * NC;
 #pragma unroll
           for (int q = 0; q < M; ++q)
-            tma_load_4d(st + q * kConsumers * kRowStrideContig, maps.ld, cx, cy, cz, q, &full[s]);
+            tma_load_4d(st + q * kConsumers * kRowStrideContig, map_ld, cx, cy, cz, q, &full[s]);
         }
       }
     }
@@ -254,16 +332,17 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const TmaMap
   mr.smax = T(0);
   mr.fin = 0xffffffffu;
   mr.bad = false;
+  mr.dtdx = L.dtdx;
   const T* pin;
   T* pout;
   if (CONTIG) {
     const int64_t off = (pb + (active ? t : 0)) * a.t1stride + (int64_t)blockIdx.z * a.t2stride;
-    pin = a.qin + off;
-    pout = a.qout + off;
+    pin = L.qin + off;
+    pout = L.qout + off;
   } else {
     const int64_t off = pb + (active ? t : 0) + (int64_t)blockIdx.z * a.t2stride;
-    pin = a.qin + off;
-    pout = a.qout + off;
+    pin = L.qin + off;
+    pout = L.qout + off;
   }
   const bool halo_lo = a.bc_lo == BC_HALO, halo_hi = a.bc_hi == BC_HALO;
   const bool refl_lo = a.bc_lo == BC_REFLECTIVE, refl_hi = a.bc_hi == BC_REFLECTIVE;
@@ -292,11 +371,9 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const TmaMap
         bool neg;
         const int js = remap(j, a.n, a.bc_lo, a.bc_hi, neg);
 #pragma unroll
-        for (int q = 0; q < M; ++q) {
-          T v = pin[js + q * a.sstride];
-          if (neg && q == a.nv) v = -v;
-          *reinterpret_cast<T*>(st + (q * kConsumers + t) * kRowStrideContig + c * (int)sizeof(T)) = v;
-        }
+        for (int q = 0; q < M; ++q)
+          *reinterpret_cast<T*>(st + (q * kConsumers + t) * kRowStrideContig + c * (int)sizeof(T)) =
+              neg_if(pin[js + q * a.sstride], neg && q == a.nv);
       }
     } else {
       const bool any = (jlo < 0 && refl_lo) || (jlo + NC > a.n && refl_hi);
@@ -362,7 +439,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const TmaMap
       const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
 #pragma unroll
       for (int q = 0; q < M; ++q)
-        tma_store_4d(maps.st, ob + q * kConsumers * kRowStrideContig, cx, cy, cz, q);
+        tma_store_4d(map_st, ob + q * kConsumers * kRowStrideContig, cx, cy, cz, q);
       bulk_commit();
     }
     flushed = tile;
@@ -445,6 +522,8 @@ __device__ __forceinline__ int segment_stages(const SweepArgs<T>& a) {
 template <typename T, class S, int LIM, bool LIT, bool CONTIG>
 __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
     sweep_kernel(const SweepArgs<T> a, const __grid_constant__ TmaMaps maps) {
+  Live<T> L;
+  if (!resolve_live(a, L)) return;
   using G = StageGeom<T, S, CONTIG>;
   constexpr int NSTAGE = G::NSTAGE;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -464,15 +543,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
   uint32_t fin = 0xffffffffu;
   bool bad = false;
   if (LIT) {
-    segment_pass<T, S, LIM, LIT, CONTIG, ExactArith>(a, maps, smem, full, empty, 0, smax, fin, bad);
+    segment_pass<T, S, LIM, LIT, CONTIG, ExactArith>(a, L, maps, smem, full, empty, 0, smax, fin, bad);
   } else {
-    segment_pass<T, S, LIM, LIT, CONTIG, FastArith>(a, maps, smem, full, empty, 0, smax, fin, bad);
+    segment_pass<T, S, LIM, LIT, CONTIG, FastArith>(a, L, maps, smem, full, empty, 0, smax, fin, bad);
     if (__syncthreads_or(bad)) {
       smax = T(0);
       fin = 0xffffffffu;
       const int k0 = segment_stages<T, S, CONTIG>(a);
-      segment_pass<T, S, LIM, LIT, CONTIG, ExactArith>(a, maps, smem, full, empty, k0, smax, fin,
-                                                       bad);
+      segment_pass<T, S, LIM, LIT, CONTIG, ExactArith>(a, L, maps, smem, full, empty, k0, smax,
+                                                       fin, bad);
     }
   }
   finish_block<T>(smax, fin, a);
@@ -485,7 +564,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
 // handed over with __shfl_sync (the two lanes that cross a chunk boundary
 // take their neighbours from a per-warp shared-memory carry slot).  Loads
 // and stores are fully coalesced.
+#ifdef CLB_PLAIN_LD
+template <typename T> __device__ __forceinline__ T ld_nc(const T* p) { return *p; }
+#else
 template <typename T> __device__ __forceinline__ T ld_nc(const T* p) { return __ldg(p); }
+#endif
 
 template <typename T, int M>
 __device__ __forceinline__ void load_cell(const T* base, int64_t sstride, int64_t astride, int j,
@@ -494,12 +577,7 @@ __device__ __forceinline__ void load_cell(const T* base, int64_t sstride, int64_
   const int js = remap(j, a.n, a.bc_lo, a.bc_hi, neg);
   const T* p = base + (int64_t)js * astride;
 #pragma unroll
-  for (int k = 0; k < M; ++k) q[k] = ld_nc(p + k * sstride);
-  if (neg) {
-#pragma unroll
-    for (int k = 0; k < M; ++k)
-      if (k == a.nv) q[k] = -q[k];
-  }
+  for (int k = 0; k < M; ++k) q[k] = neg_if(ld_nc(p + k * sstride), neg && k == a.nv);
 }
 
 template <typename T, class S> struct CarryLayout {
@@ -512,6 +590,8 @@ template <typename T, class S> struct CarryLayout {
 // Axis 0 (contiguous): warp-marching kernel.
 template <typename T, class S, int LIM, bool LIT>
 __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
+  Live<T> L;
+  if (!resolve_live(a, L)) return;
   const int lim_id = LIM >= 0 ? LIM : a.lim_id;
   using Cell = typename S::Cell;
   using Fan = typename S::Fan;
@@ -533,15 +613,28 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
     const int y = (int)(row % a.n1);
     const int z = (int)(row / a.n1);
     const int64_t off = (int64_t)y * a.t1stride + (int64_t)z * a.t2stride;
-    const T* qrow = a.qin + off;
-    T* orow = a.qout + off;
+    const T* qrow = L.qin + off;
+    T* orow = L.qout + off;
     const int lo = seg * a.seg_len;
     const int hi = min(a.n, lo + a.seg_len);
 
+    // software pipeline: the cells of the next kPrefetch chunks are already
+    // in flight while this chunk marches (the loop was load-latency bound)
+    constexpr int kPrefetch = 2;
+    T qp[kPrefetch][M];
+#pragma unroll
+    for (int j = 0; j < kPrefetch; ++j)
+      load_cell<T, M>(qrow, a.sstride, 1, min(lo - 2 + 32 * j + lane, hi + 1), a, qp[j]);
     for (int b = lo - 2; b <= hi + 1; b += 32) {
       const int x = b + lane;
       T q[M];
-      load_cell<T, M>(qrow, a.sstride, 1, min(x, hi + 1), a, q);
+#pragma unroll
+      for (int k = 0; k < M; ++k) q[k] = qp[0][k];
+#pragma unroll
+      for (int j = 0; j + 1 < kPrefetch; ++j)
+#pragma unroll
+        for (int k = 0; k < M; ++k) qp[j][k] = qp[j + 1][k];
+      load_cell<T, M>(qrow, a.sstride, 1, min(x + 32 * kPrefetch, hi + 1), a, qp[kPrefetch - 1]);
       bool bad_ = false;
       Cell c = S::template make<ExactArith>(q, bad_);
 
@@ -567,7 +660,7 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
         S::for_regs(F2, [&](T& r) { r = carry[wib][lane][i++]; });
       }
       T G[M];
-      correction<S, LIT, ExactArith, T>(F2, F1, F, a.P, a.dtdx, lim_id, G, bad_);
+      correction<S, LIT, ExactArith, T>(F2, F1, F, a.P, L.dtdx, lim_id, G, bad_);
       T G1[M], q2[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) {
@@ -584,7 +677,7 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
       }
       if (x >= lo + 2 && x <= hi + 1) {
         T o[M];
-        update<S, LIT, T>(q2, F2, F1, G, G1, a.P, a.dtdx, o);
+        update<S, LIT, T>(q2, F2, F1, G, G1, a.P, L.dtdx, o);
         T* dst = orow + (x - 2);
 #pragma unroll
         for (int k = 0; k < M; ++k) {
@@ -632,7 +725,12 @@ __global__ void solve_pairs(const T* ql, const T* qr, T* W, T* s, int64_t n, Par
 // Launch plumbing shared by the instantiation units.
 
 struct GenericArgs {
-  const TmaMaps* maps;  // contig TMA sweep only
+  const TmaMaps* maps;  // all three buffers' maps (contig TMA sweep only)
+  int src, dst;
+  const DevCtl* ctl;    // indirect launch (batch graphs)
+  int axis;
+  double spacing;
+  const void* bufs[3];
   int tx0, ty0, tz0;
   const void* qin;
   void* qout;
@@ -662,6 +760,11 @@ inline SweepArgs<T> to_args(const GenericArgs& g) {
   a.smax_bits = g.smax_bits;
   a.nonfinite = g.nonfinite;
   a.tx0 = g.tx0; a.ty0 = g.ty0; a.tz0 = g.tz0;
+  a.src = g.src; a.dst = g.dst;
+  a.ctl = g.ctl;
+  a.axis = g.axis;
+  a.spacing = g.spacing;
+  for (int i = 0; i < 3; ++i) a.bufs[i] = g.bufs[i];
   return a;
 }
 

@@ -369,3 +369,79 @@ def test_slow_path_inputs_match_oracle(rng, limiter, dtype):
                        {"gravity": 1.0})
         assert out.interior().tobytes() == O.interior(ref).tobytes()
         assert res.max_abs_speed == smax
+
+
+# ---------------------------------------------------------------------------
+# Device-resident controller (clb_run_batch): run_until's attempt loop on the
+# device must reproduce the host loop exactly -- attempts, reverts, frames,
+# final state, counters and exceptions.
+
+def _both_modes(r, cap=4096, **kw):
+    out = []
+    for dc in (False, True):
+        sim, _ = cases.product_sim(r, device_controller=dc)
+        sim._batch_log_cap = cap
+        frames = []
+        with sim:
+            rep = sim.run_until(r["drive"][1], frame_times=tuple(r["drive"][2]),
+                                on_frame=lambda s: frames.append((s.t, cases.sha(s.grid.interior())))) \
+                if r["drive"][0] == "until" else sim.run_until(1e30, max_steps=r["drive"][1])
+            out.append((cases.attempts_hex(rep.attempts), [a.dt_retry for a in rep.attempts],
+                        rep.steps_accepted, rep.steps_reverted, float(rep.nu_max).hex(),
+                        float(rep.t_final).hex(), frames, cases.sha(sim.grid.interior()),
+                        sim.steps_accepted, sim.steps_reverted, float(sim.last_max_speed).hex(),
+                        sim._prev_reverted, float(sim.nu_max).hex()))
+    return out
+
+
+@pytest.mark.parametrize("name", sorted(cases.RECIPES))
+@pytest.mark.parametrize("cap", [4096, 3])
+def test_device_controller_matches_host_loop(name, cap):
+    host, dev = _both_modes(cases.RECIPES[name], cap)
+    assert dev == host
+
+
+def test_device_controller_reverts_and_frames():
+    r = dict(cases.RECIPES["dam_break_revert_64x16"])
+    r["drive"] = ("until", 0.15, (0.01, 0.05, 0.1))
+    host, dev = _both_modes(r)
+    assert dev == host
+    assert host[3] >= 1 and len(host[6]) == 3
+
+
+def test_device_controller_unstable_step_error():
+    spec = P.GridSpec((8, 8), (0, 0), (1, 1), 3)
+    msgs = []
+    for dc in (False, True):
+        g = P.create_grid(spec)
+        g.data[0] = 4.0
+        sim = P.Simulation(g, P.get_solver("shallow_water"), P.ShallowWaterParams(1.0),
+                           P.BoundarySpec.uniform(P.BoundaryKind.PERIODIC, (1, 2)),
+                           initial_max_speed=1.0, device_controller=dc)
+        sim.attempt_step()                       # revert (nu = 1.8)
+        sim.last_max_speed = 1.0                 # engineered under-estimate again
+        with pytest.raises(P.UnstableStepError) as exc:
+            sim.run_until(1.0)
+        msgs.append((str(exc.value), sim.steps_reverted, float(sim.last_max_speed).hex()))
+        sim.close()
+    assert msgs[0] == msgs[1]
+
+
+@pytest.mark.parametrize("where", [(3, 4), (15, 0)])
+def test_device_controller_blowup_location(where):
+    spec = P.GridSpec((16, 16), (0, 0), (1, 1), 3)
+    base = 0.05 * np.random.default_rng(1).standard_normal((3, 16, 16))
+    res = []
+    for dc in (False, True):
+        g = P.create_grid(spec)
+        g.interior()[...] = base
+        sim = P.Simulation(g, P.get_solver("acoustics"), P.AcousticsParams(),
+                           P.BoundarySpec.uniform(P.BoundaryKind.PERIODIC, (1, 2)),
+                           initial_max_speed=1.0, device_controller=dc)
+        sim.run_until(1e30, max_steps=3)
+        sim.grid.interior(0)[where] = np.inf
+        with pytest.raises(P.NumericalBlowup) as exc:
+            sim.run_until(1e30, max_steps=5)
+        res.append((exc.value.state, exc.value.cell, exc.value.step, sim.steps_accepted))
+        sim.close()
+    assert res[0] == res[1]
