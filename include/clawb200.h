@@ -19,6 +19,7 @@
  *   clb_run_batch              Simulation.run_until's attempt loop  timestep.py:245-285
  *                              with estimate_dt / attempt_step      timestep.py:151-243
  *                              evaluated on the device (fp64, same expressions)
+ *   clb_write_frame            frames.frame_bytes / write_frame     frames.py:74-104
  *   clb_first_nonfinite        Simulation._check_finite             timestep.py:179-186
  *   clb_solve_pairs            RiemannSolver.solve                  riemann.py:205-223
  *   clb_last_error             (exceptions never cross the ABI)
@@ -160,6 +161,13 @@ int clb_halo_copy(clb_handle h, int buf, int side, int to_host, void *host);
  * W out (n, nw, m), s out (n, nw). */
 int clb_solve_pairs(clb_handle h, int axis, int64_t n, const void *ql, const void *qr,
                     void *W, void *s);
+
+/* Frame writer (frames.py:1-104 CLAWFRM1): header + the interior payload of
+ * buffer `buf` (per state, x fastest, ghost cells excluded), written straight
+ * into `out` (pinned memory gives a direct device->host copy).  The bytes
+ * equal frame_bytes(grid, time, step) of the reference. */
+int clb_frame_size(clb_handle h, size_t *nbytes);
+int clb_write_frame(clb_handle h, int buf, double time, uint64_t step, void *out, size_t nbytes);
 
 /* Device-resident run loop (timestep.py:245-285 run_until between two stop
  * times).  Attempts run back to back from a CUDA graph: the ndim sweeps read

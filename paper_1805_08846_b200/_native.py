@@ -34,7 +34,7 @@ EXPORTS = (
     "clb_download_padded", "clb_set_boundary", "clb_sweep", "clb_sweep_async", "clb_fetch",
     "clb_attempt_step", "clb_first_nonfinite", "clb_halo_layout", "clb_halo_copy", "clb_solve_pairs",
     "clb_enable_timing", "clb_timing", "clb_host_alloc", "clb_host_free", "clb_memory_info",
-    "clb_selftest_arith", "clb_run_batch",
+    "clb_selftest_arith", "clb_run_batch", "clb_frame_size", "clb_write_frame",
 )
 
 #: clb_run_batch statuses (include/clawb200.h)
@@ -131,6 +131,8 @@ def lib():
         "clb_memory_info": (_int, [_vp, ctypes.POINTER(_sz), ctypes.POINTER(_i64)]),
         "clb_selftest_arith": (_int, [_int, _i64, _vp, _vp, ctypes.POINTER(_i64)]),
         "clb_run_batch": (_int, [_vp, ctypes.POINTER(ClbBatch), ctypes.POINTER(ClbAttempt), _i64]),
+        "clb_frame_size": (_int, [_vp, ctypes.POINTER(_sz)]),
+        "clb_write_frame": (_int, [_vp, _int, _dbl, ctypes.c_uint64, _vp, _sz]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -314,6 +316,19 @@ class DeviceGrid:
         log = (ClbAttempt * log_cap)()
         _check(lib().clb_run_batch(self.handle, ctypes.byref(batch), log, log_cap), self.handle)
         return [log[i] for i in range(batch.n_attempts)]
+
+    def frame_size(self) -> int:
+        n = _sz()
+        _check(lib().clb_frame_size(self.handle, ctypes.byref(n)), self.handle)
+        return n.value
+
+    def write_frame(self, buf: int, time: float, step: int, out) -> None:
+        """CLAWFRM1 frame of buffer `buf` into the writable buffer `out`
+        (e.g. a PinnedBuffer's array) of exactly frame_size() bytes."""
+        mv = memoryview(out).cast("B")
+        addr = ctypes.addressof(ctypes.c_char.from_buffer(mv))
+        _check(lib().clb_write_frame(self.handle, buf, float(time), int(step), addr, mv.nbytes),
+               self.handle)
 
     def enable_timing(self, on: bool = True):
         _check(lib().clb_enable_timing(self.handle, 1 if on else 0), self.handle)

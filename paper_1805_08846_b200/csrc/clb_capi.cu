@@ -175,8 +175,9 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   g.num_sms = h->num_sms;
   const int64_t nx = h->cells[0], ny = h->cells[1], nz = h->cells[2];
   // Work decomposition: 128 pencils per CTA; segments along the sweep axis
-  // until ~6 CTAs per SM are in flight, but never shorter than 32 cells (each
-  // segment re-reads 4 cells and re-solves 3 fans of its neighbour).
+  // until ~6 CTAs per SM are in flight, but never shorter than 16 cells (each
+  // segment re-reads 4 cells and re-solves 3 fans of its neighbour;
+  // CLB_MIN_SEG overrides, profiles/r1_notes.md).
   const int64_t target_ctas = (int64_t)h->num_sms * 6;
   int64_t pen_ctas;
   // x-sweep kernel: the TMA tensor-map variant wins when the march is
@@ -215,7 +216,7 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   int64_t nseg = (target_ctas + pen_ctas - 1) / pen_ctas;
   static const int64_t min_seg = [] {
     const char* e = getenv("CLB_MIN_SEG");
-    return e ? std::max<int64_t>(4, atoll(e)) : (int64_t)32;
+    return e ? std::max<int64_t>(4, atoll(e)) : (int64_t)16;
   }();
   nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, g.n / min_seg));
   int64_t L = (g.n + nseg - 1) / nseg;
@@ -613,6 +614,43 @@ int clb_upload(clb_handle h, int buf, const void* src, size_t nbytes) {
 int clb_download(clb_handle h, int buf, void* dst, size_t nbytes) {
   return transfer(h, buf, dst, nbytes, false, false);
 }
+// frames.py:1-18 CLAWFRM1 header: magic, u32 version, u32 ndim, u32 dims[ndim]
+// (x first), u32 num_states, u32 precision, f64 time, u64 step; little-endian,
+// no padding.  The payload is exactly clb_download's interior order.
+static size_t frame_header_size(const clb_ctx* h) { return 8 + 4 + 4 + 4 * h->ndim + 4 + 4 + 8 + 8; }
+
+int clb_frame_size(clb_handle h, size_t* nbytes) {
+  if (!h || !nbytes) return fail(h, CLB_EINVAL, "null argument");
+  size_t payload = (size_t)h->M * h->itemsize;
+  for (int ax = 0; ax < h->ndim; ++ax) payload *= (size_t)h->cells[ax];
+  *nbytes = frame_header_size(h) + payload;
+  return CLB_OK;
+}
+
+int clb_write_frame(clb_handle h, int buf, double time, uint64_t step, void* out, size_t nbytes) {
+  if (!h || !out) return fail(h, CLB_EINVAL, "null argument");
+  size_t want = 0;
+  clb_frame_size(h, &want);
+  if (nbytes != want) return fail(h, CLB_EINVAL, "byte count does not match the frame size");
+  unsigned char* p = (unsigned char*)out;
+  auto put = [&p](const void* v, size_t n) { std::memcpy(p, v, n); p += n; };
+  static_assert(sizeof(double) == 8, "f64");
+  put("CLAWFRM1", 8);
+  const uint32_t version = 1, ndim = (uint32_t)h->ndim;
+  put(&version, 4);
+  put(&ndim, 4);
+  for (int ax = 0; ax < h->ndim; ++ax) {
+    const uint32_t d = (uint32_t)h->cells[ax];
+    put(&d, 4);
+  }
+  const uint32_t m = (uint32_t)h->M, isz = (uint32_t)h->itemsize;
+  put(&m, 4);
+  put(&isz, 4);
+  put(&time, 8);
+  put(&step, 8);
+  return transfer(h, buf, p, nbytes - frame_header_size(h), false, false);
+}
+
 int clb_upload_padded(clb_handle h, int buf, const void* src, size_t nbytes) {
   return transfer(h, buf, const_cast<void*>(src), nbytes, true, true);
 }

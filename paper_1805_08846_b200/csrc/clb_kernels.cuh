@@ -618,23 +618,10 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
     const int lo = seg * a.seg_len;
     const int hi = min(a.n, lo + a.seg_len);
 
-    // software pipeline: the cells of the next kPrefetch chunks are already
-    // in flight while this chunk marches (the loop was load-latency bound)
-    constexpr int kPrefetch = 2;
-    T qp[kPrefetch][M];
-#pragma unroll
-    for (int j = 0; j < kPrefetch; ++j)
-      load_cell<T, M>(qrow, a.sstride, 1, min(lo - 2 + 32 * j + lane, hi + 1), a, qp[j]);
     for (int b = lo - 2; b <= hi + 1; b += 32) {
       const int x = b + lane;
       T q[M];
-#pragma unroll
-      for (int k = 0; k < M; ++k) q[k] = qp[0][k];
-#pragma unroll
-      for (int j = 0; j + 1 < kPrefetch; ++j)
-#pragma unroll
-        for (int k = 0; k < M; ++k) qp[j][k] = qp[j + 1][k];
-      load_cell<T, M>(qrow, a.sstride, 1, min(x + 32 * kPrefetch, hi + 1), a, qp[kPrefetch - 1]);
+      load_cell<T, M>(qrow, a.sstride, 1, min(x, hi + 1), a, q);
       bool bad_ = false;
       Cell c = S::template make<ExactArith>(q, bad_);
 
