@@ -92,7 +92,8 @@ const char *clb_last_error(clb_handle h);
 int clb_version(void);
 
 /* Optional: run on a caller-owned cudaStream_t (e.g. torch's current stream
- * for NCCL ordering).  NULL restores the handle's own stream. */
+ * for NCCL ordering); cudaStreamLegacy ((void*)1) selects the legacy default
+ * stream.  NULL restores the handle's own stream. */
 int clb_set_stream(clb_handle h, void *cuda_stream);
 
 /* Segment length (cells along the sweep axis per warp/thread) for one

@@ -303,7 +303,12 @@ class Slab:
 
 
 def _torch_stream():
+    """Torch's current stream as a handle for clb_set_stream.  Torch reports
+    its legacy default stream as 0, which the library would read as "use
+    your own stream" (unordered with torch's NCCL work); pass
+    cudaStreamLegacy (0x1) instead so the sweeps and the halo/max-allreduce
+    collectives stay in one order."""
     import torch
-    return torch.cuda.current_stream().cuda_stream
+    return torch.cuda.current_stream().cuda_stream or 0x1
 
 
