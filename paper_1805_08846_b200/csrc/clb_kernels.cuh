@@ -586,6 +586,58 @@ template <typename T, class S> struct CarryLayout {
   static constexpr int kAll = kCell + kFan + S::M;
 };
 
+// One 32-cell chunk of the warp-marching x sweep under arithmetic policy D:
+// lane l owns cell x = b + l.  Pure: reads the loaded cell and the warp's
+// carry slots, writes only (c, F, G, o).  In a row's first chunk lanes 0-1
+// keep their shuffled (real but unrelated) neighbours instead of the
+// not-yet-written carry; their results are never used, and real data cannot
+// fake a slow-path flag.
+template <typename T, class S, bool LIT, class D>
+__device__ __forceinline__ void contig_chunk(
+    const SweepArgs<T>& a, T dtdx, int lim_id, const T (&q)[S::M], bool first, int lane,
+    T (&carry)[2][CarryLayout<T, S>::kAll], typename S::Cell& c, typename S::Fan& F,
+    T (&G)[S::M], T (&o)[S::M], bool& bad) {
+  using Cell = typename S::Cell;
+  using Fan = typename S::Fan;
+  constexpr int M = S::M;
+  constexpr int KC = CarryLayout<T, S>::kCell, KF = CarryLayout<T, S>::kFan;
+  c = S::template make<D>(q, bad);
+  Cell cl = c;
+  S::for_cell_regs(cl, [&](T& r) { r = __shfl_sync(FULL, r, (lane + 31) & 31); });
+  if (lane == 0 && !first) {
+    int i = 0;
+    S::for_cell_regs(cl, [&](T& r) { r = carry[1][i++]; });
+  }
+  F = S::template solve<D>(cl, c, a.P, bad);
+  Fan F1 = F, F2 = F;
+  S::for_regs(F1, [&](T& r) { r = __shfl_sync(FULL, r, (lane + 31) & 31); });
+  S::for_regs(F2, [&](T& r) { r = __shfl_sync(FULL, r, (lane + 30) & 31); });
+  if (lane == 0 && !first) {
+    int i = KC;
+    S::for_regs(F1, [&](T& r) { r = carry[1][i++]; });
+  }
+  if (lane < 2 && !first) {
+    int i = KC;
+    S::for_regs(F2, [&](T& r) { r = carry[lane][i++]; });
+  }
+  correction<S, LIT, D, T>(F2, F1, F, a.P, dtdx, lim_id, G, bad);
+  T G1[M], q2[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    G1[k] = __shfl_sync(FULL, G[k], (lane + 31) & 31);
+    q2[k] = __shfl_sync(FULL, c.q[k], (lane + 30) & 31);
+  }
+  if (lane == 0 && !first) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) G1[k] = carry[1][KC + KF + k];
+  }
+  if (lane < 2 && !first) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) q2[k] = carry[lane][k];  // Cell starts with q[M]
+  }
+  update<S, LIT, T>(q2, F2, F1, G, G1, a.P, dtdx, o);
+}
+
 // ---------------------------------------------------------------------------
 // Axis 0 (contiguous): warp-marching kernel.
 template <typename T, class S, int LIM, bool LIT>
@@ -620,51 +672,33 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
 
     for (int b = lo - 2; b <= hi + 1; b += 32) {
       const int x = b + lane;
+      const bool first = b == lo - 2;
       T q[M];
       load_cell<T, M>(qrow, a.sstride, 1, min(x, hi + 1), a, q);
-      bool bad_ = false;
-      Cell c = S::template make<ExactArith>(q, bad_);
-
-      // left neighbour cell (x-1)
-      Cell cl = c;
-      S::for_cell_regs(cl, [&](T& r) { r = __shfl_sync(FULL, r, (lane + 31) & 31); });
-      if (lane == 0) {
-        int i = 0;
-        S::for_cell_regs(cl, [&](T& r) { r = carry[wib][1][i++]; });
+      Cell c;
+      Fan F;
+      T G[M], o[M];
+      bool bad = false;
+      // fp32: the exact branchy division (zero numerators short-cut) measured
+      // faster in this kernel than the fp64-pipe fast path
+      if (LIT || sizeof(T) == 4) {
+        contig_chunk<T, S, LIT, ExactArith>(a, L.dtdx, lim_id, q, first, lane, carry[wib], c, F, G,
+                                            o, bad);
+      } else {
+        // branch-free IEEE arithmetic; a chunk in which any lane left the
+        // fast-path domain is recomputed exactly (its inputs -- loaded cells
+        // and the carry -- are untouched until the commit below)
+        contig_chunk<T, S, LIT, FastArith>(a, L.dtdx, lim_id, q, first, lane, carry[wib], c, F, G,
+                                           o, bad);
+        if (__any_sync(FULL, bad)) {
+          bad = false;
+          contig_chunk<T, S, LIT, ExactArith>(a, L.dtdx, lim_id, q, first, lane, carry[wib], c, F,
+                                              G, o, bad);
+        }
       }
-      Fan F = S::template solve<ExactArith>(cl, c, a.P, bad_);
+      // commit: max |s|, outputs, carry
       if (x >= lo - 1 && x <= hi + 1) fold_speed<S, T>(F, a.P, smax);
-
-      Fan F1 = F, F2 = F;
-      S::for_regs(F1, [&](T& r) { r = __shfl_sync(FULL, r, (lane + 31) & 31); });
-      S::for_regs(F2, [&](T& r) { r = __shfl_sync(FULL, r, (lane + 30) & 31); });
-      if (lane == 0) {
-        int i = KC;
-        S::for_regs(F1, [&](T& r) { r = carry[wib][1][i++]; });
-      }
-      if (lane < 2) {
-        int i = KC;
-        S::for_regs(F2, [&](T& r) { r = carry[wib][lane][i++]; });
-      }
-      T G[M];
-      correction<S, LIT, ExactArith, T>(F2, F1, F, a.P, L.dtdx, lim_id, G, bad_);
-      T G1[M], q2[M];
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        G1[k] = __shfl_sync(FULL, G[k], (lane + 31) & 31);
-        q2[k] = __shfl_sync(FULL, c.q[k], (lane + 30) & 31);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < M; ++k) G1[k] = carry[wib][1][KC + KF + k];
-      }
-      if (lane < 2) {
-#pragma unroll
-        for (int k = 0; k < M; ++k) q2[k] = carry[wib][lane][k];  // Cell starts with q[M]
-      }
       if (x >= lo + 2 && x <= hi + 1) {
-        T o[M];
-        update<S, LIT, T>(q2, F2, F1, G, G1, a.P, L.dtdx, o);
         T* dst = orow + (x - 2);
 #pragma unroll
         for (int k = 0; k < M; ++k) {
