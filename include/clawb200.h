@@ -131,6 +131,16 @@ int clb_sweep_async(clb_handle h, int axis, double dt, int src, int dst, int slo
                     int literal);
 int clb_fetch(clb_handle h, int nslots, double *max_abs_speed, int32_t *nonfinite);
 
+/* Segment decomposition of a strided sweep along its axis (nseg segments of
+ * seg_len cells; the contiguous x sweep reports one segment), and a launch
+ * of segments [seg_begin, seg_end) only.  Segment k reads rows
+ * [k*seg_len - 2, min(n, (k+1)*seg_len) + 2), so the segments that stay
+ * clear of the ghost rows can run while a halo exchange is in flight
+ * (multi-GPU overlap); results are bitwise those of one full launch. */
+int clb_sweep_segments(clb_handle h, int axis, int32_t *nseg, int32_t *seg_len);
+int clb_sweep_async_range(clb_handle h, int axis, double dt, int src, int dst, int slot,
+                          int literal, int seg_begin, int seg_end);
+
 /* All ndim sweeps of one step attempt, x then y then z (timestep.py:35-42,
  * 200-211): sweep j reads the previous output and writes scratch[j % 2].
  * One device->host read at the end.  speeds[j], nonfinite[j] per sweep. */

@@ -35,6 +35,7 @@ EXPORTS = (
     "clb_attempt_step", "clb_first_nonfinite", "clb_halo_layout", "clb_halo_copy", "clb_solve_pairs",
     "clb_enable_timing", "clb_timing", "clb_host_alloc", "clb_host_free", "clb_memory_info",
     "clb_selftest_arith", "clb_run_batch", "clb_frame_size", "clb_write_frame",
+    "clb_sweep_segments", "clb_sweep_async_range",
 )
 
 #: clb_run_batch statuses (include/clawb200.h)
@@ -132,6 +133,8 @@ def lib():
         "clb_selftest_arith": (_int, [_int, _i64, _vp, _vp, ctypes.POINTER(_i64)]),
         "clb_run_batch": (_int, [_vp, ctypes.POINTER(ClbBatch), ctypes.POINTER(ClbAttempt), _i64]),
         "clb_frame_size": (_int, [_vp, ctypes.POINTER(_sz)]),
+        "clb_sweep_segments": (_int, [_vp, _int, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+        "clb_sweep_async_range": (_int, [_vp, _int, _dbl, _int, _int, _int, _int, _int, _int]),
         "clb_write_frame": (_int, [_vp, _int, _dbl, ctypes.c_uint64, _vp, _sz]),
     }
     for name, (res, args) in sig.items():
@@ -256,6 +259,18 @@ class DeviceGrid:
                     literal: bool = False):
         _check(lib().clb_sweep_async(self.handle, axis, float(dt), src, dst, slot,
                                      1 if literal else 0), self.handle)
+
+    def segments(self, axis: int):
+        """(nseg, seg_len) of the sweep along `axis`."""
+        n, L = _i32(0), _i32(0)
+        _check(lib().clb_sweep_segments(self.handle, axis, ctypes.byref(n), ctypes.byref(L)),
+               self.handle)
+        return int(n.value), int(L.value)
+
+    def sweep_async_range(self, axis: int, dt: float, src: int, dst: int, slot: int,
+                          seg_begin: int, seg_end: int, literal: bool = False):
+        _check(lib().clb_sweep_async_range(self.handle, axis, float(dt), src, dst, slot,
+                                           1 if literal else 0, seg_begin, seg_end), self.handle)
 
     def fetch(self, nslots: int):
         s = (_dbl * 4)()

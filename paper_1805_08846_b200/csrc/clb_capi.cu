@@ -224,12 +224,14 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   L = (L + align - 1) / align * align;
   g.seg_len = (int)L;
   g.nseg = (int)((g.n + L - 1) / L);
+  g.seg_begin = 0;
+  g.seg_end = g.nseg;
   return g;
 }
 
 // indirect: buffers and dt are read by the kernel from h->d_ctl (batch graphs)
 int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bool literal,
-                 bool indirect = false) {
+                 bool indirect = false, int seg_begin = 0, int seg_end = -1) {
   if (axis < 0 || axis >= h->ndim) return fail(h, CLB_EINVAL, "sweep axis out of range");
   if (src < 0 || src > 2 || dst < 0 || dst > 2) return fail(h, CLB_EINVAL, "buffer index out of range");
   if (src == dst) return fail(h, CLB_EINVAL, "sweep cannot run in place");
@@ -237,6 +239,13 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
   if (slot < 0 || slot > 3) return fail(h, CLB_EINVAL, "result slot out of range");
   clb::GenericArgs g = sweep_geometry(h, axis, src, dst);
   g.ctl = indirect ? h->d_ctl : nullptr;
+  if (seg_end >= 0) {
+    if (g.contig) return fail(h, CLB_EINVAL, "segment ranges apply to strided sweeps only");
+    if (seg_begin < 0 || seg_end > g.nseg || seg_begin >= seg_end)
+      return fail(h, CLB_EINVAL, "segment range out of bounds");
+    g.seg_begin = seg_begin;
+    g.seg_end = seg_end;
+  }
   // sweep.py:336-337: dtdx = T(dt / dx[axis]) -- fp64 divide, then round to T.
   const double dtdx64 = dt / h->d.spacing[axis];
   g.dtdx = h->itemsize == 8 ? dtdx64 : (double)(float)dtdx64;
@@ -661,6 +670,21 @@ int clb_download_padded(clb_handle h, int buf, void* dst, size_t nbytes) {
 int clb_sweep_async(clb_handle h, int axis, double dt, int src, int dst, int slot, int literal) {
   if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
   return launch_sweep(h, axis, dt, src, dst, slot, literal != 0);
+}
+
+int clb_sweep_segments(clb_handle h, int axis, int32_t* nseg, int32_t* seg_len) {
+  if (!h || !nseg || !seg_len) return fail(h, CLB_EINVAL, "null argument");
+  if (axis < 0 || axis >= h->ndim) return fail(h, CLB_EINVAL, "sweep axis out of range");
+  const clb::GenericArgs g = sweep_geometry(h, axis, 0, 1);
+  *nseg = g.contig ? 1 : g.nseg;
+  *seg_len = g.contig ? (int32_t)g.n : g.seg_len;
+  return CLB_OK;
+}
+
+int clb_sweep_async_range(clb_handle h, int axis, double dt, int src, int dst, int slot,
+                          int literal, int seg_begin, int seg_end) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  return launch_sweep(h, axis, dt, src, dst, slot, literal != 0, false, seg_begin, seg_end);
 }
 
 int clb_fetch(clb_handle h, int nslots, double* speeds, int32_t* nonfinite) {

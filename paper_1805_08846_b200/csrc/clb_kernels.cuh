@@ -69,6 +69,7 @@ template <typename T> struct SweepArgs {
   int n;            // cells along the sweep axis
   int n1, n2;       // transverse extents
   int seg_len, nseg;
+  int seg_base;     // first segment of this launch (segment-range launches)
   int bc_lo, bc_hi, nv;
   int lim_id;
   T dtdx;
@@ -271,7 +272,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   const unsigned char* map_st = maps_all.st[L.dst];
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int seg = blockIdx.y;
+  const int seg = blockIdx.y + a.seg_base;
   const int lo = seg * a.seg_len;
   const int hi = min(a.n, lo + a.seg_len);
   const int ncell = hi - lo + A + 4;
@@ -503,7 +504,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 template <typename T, class S, bool CONTIG>
 __device__ __forceinline__ int segment_stages(const SweepArgs<T>& a) {
   using G = StageGeom<T, S, CONTIG>;
-  const int lo = blockIdx.y * a.seg_len;
+  const int lo = (blockIdx.y + a.seg_base) * a.seg_len;
   const int hi = min(a.n, lo + a.seg_len);
   return (hi - lo + G::A + 4 + G::NC - 1) / G::NC;
 }
@@ -764,6 +765,7 @@ struct GenericArgs {
   int* nonfinite;
   int contig;         // 1: axis-0 (x) sweep, warp-marching; 2: axis 0, TMA transpose
   int seg_len, nseg;
+  int seg_begin, seg_end;  // segment range of this launch (strided kernels)
   int num_sms;
 };
 
@@ -775,6 +777,7 @@ inline SweepArgs<T> to_args(const GenericArgs& g) {
   a.sstride = g.sstride; a.astride = g.astride; a.t1stride = g.t1stride; a.t2stride = g.t2stride;
   a.n = g.n; a.n1 = g.n1; a.n2 = g.n2;
   a.seg_len = g.seg_len; a.nseg = g.nseg;
+  a.seg_base = g.seg_begin;
   a.bc_lo = g.bc_lo; a.bc_hi = g.bc_hi; a.nv = g.nv; a.lim_id = g.lim_id;
   a.dtdx = (T)g.dtdx;
   for (int i = 0; i < 4; ++i) a.P.p[i] = (T)g.params[i];
@@ -811,7 +814,8 @@ inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
   }
   SweepArgs<T> a = to_args<T>(g);
   static const TmaMaps none{};
-  dim3 grid((unsigned)((g.n1 + kConsumers - 1) / kConsumers), (unsigned)g.nseg, (unsigned)g.n2);
+  dim3 grid((unsigned)((g.n1 + kConsumers - 1) / kConsumers), (unsigned)(g.seg_end - g.seg_begin),
+            (unsigned)g.n2);
   fn<<<grid, kThreads, Geo::SMEM, st>>>(a, CONTIG ? *g.maps : none);
   return cudaGetLastError();
 }

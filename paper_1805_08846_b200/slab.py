@@ -12,6 +12,9 @@ multi-GPU path the north star asks for without changing the arithmetic:
   rows into its own ghost layers (``CLB_BC_HALO``), a periodic slow axis
   wrapping rank 0 <-> P-1; the global physical boundary on the slow axis
   is synthesised by ranks 0 and P-1 only;
+* the exchange overlaps the slow sweep: the sweep's segments that read no
+  ghost row are launched while the send/recv are in flight, the edge
+  segments after they land (``slow_sweep``);
 * the per-sweep (max |s|, non-finite) results are max-allreduced, so every
   rank takes the identical fp64 accept/revert decision.
 
@@ -183,9 +186,16 @@ class Slab:
     def exchange(self, buf: int) -> None:
         """Fill the slow-axis ghost layers of device buffer `buf` from the
         neighbours' boundary rows/planes (both sides, every state)."""
+        self.exchange_end(self.exchange_begin(buf))
+
+    def exchange_begin(self, buf: int):
+        """Post the halo exchange of `buf`.  NCCL: the send/recv run on the
+        collective stream behind the work already queued (the sweep that
+        produced `buf`) and this returns at once; host transport: done on
+        return.  Pass the result to exchange_end."""
         L = self.layout
         if L.world == 1 or (L.lo_nbr is None and L.hi_nbr is None):
-            return
+            return None
         m = self.global_spec.num_states
         self._buf = buf
         sides = []
@@ -198,9 +208,19 @@ class Slab:
             else:
                 sides.append((side, nbr))
         if self.transport == "nccl":
-            self._exchange_nccl(sides, m)
-        else:
-            self._exchange_host(sides, m)
+            return self._exchange_nccl(sides, m)
+        self._exchange_host(sides, m)
+        return None
+
+    @staticmethod
+    def exchange_end(pending) -> None:
+        """Make the library's stream wait for a posted exchange (stream-level
+        for NCCL: the host does not block)."""
+        if pending is None:
+            return
+        reqs, _keep = pending
+        for req in reqs:
+            req.wait()
 
     def _exchange_nccl(self, sides, m):
         """Zero-copy NCCL send/recv on the library's buffers.  NCCL pairs
@@ -230,8 +250,7 @@ class Slab:
                 for k in range(m):
                     ops.append(dist.P2POp(dist.irecv, view(recv + k * sstride, nbytes), nbr,
                                           group=self.group))
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        return dist.batch_isend_irecv(ops), keep
 
     def _exchange_host(self, sides, m):
         import torch
@@ -250,17 +269,48 @@ class Slab:
             self.dev.halo_write(self._buf, side, rbuf)
 
     # -- the step ------------------------------------------------------------------
+    def halo_free_segments(self, axis: int):
+        """Segments of the slow-axis sweep that read no ghost row: segment k
+        reads rows [k*L - 2, min(n, (k+1)*L) + 2) (clb_sweep_segments)."""
+        nseg, seg_len = self.dev.segments(axis)
+        n = self.layout.count
+        inner = [k for k in range(nseg)
+                 if k * seg_len >= 2 and min(n, (k + 1) * seg_len) + 2 <= n]
+        return nseg, (inner[0], inner[-1] + 1) if inner else None
+
+    def slow_sweep(self, dt: float, src: int, dst: int, slot: int, literal: bool = False):
+        """The slow-axis sweep overlapped with its halo exchange: the
+        segments clear of the ghost rows run while the exchange is in flight,
+        the two edge groups after it lands.  Bitwise the same as exchanging
+        first and sweeping once (segments are independent)."""
+        dev = self.dev
+        axis = self.layout.axis
+        pending = self.exchange_begin(src)
+        nseg, inner = self.halo_free_segments(axis)
+        if pending is None or inner is None:
+            self.exchange_end(pending)
+            dev.sweep_async(axis, dt, src, dst, slot, literal=literal)
+            return
+        b, e = inner
+        dev.sweep_async_range(axis, dt, src, dst, slot, b, e, literal=literal)
+        self.exchange_end(pending)
+        if b > 0:
+            dev.sweep_async_range(axis, dt, src, dst, slot, 0, b, literal=literal)
+        if e < nseg:
+            dev.sweep_async_range(axis, dt, src, dst, slot, e, nseg, literal=literal)
+
     def attempt_step(self, sim, dt: float):
-        """Sweeps of one attempt with the halo exchange before the slow sweep;
-        returns the max-allreduced per-sweep (speeds, nonfinite)."""
+        """Sweeps of one attempt with the halo exchange overlapping the slow
+        sweep; returns the max-allreduced per-sweep (speeds, nonfinite)."""
         dev = self.dev
         nd = len(sim.step_order)
         src = sim._cur
         for j in range(nd):
             dst = sim._scratch[j % 2]
             if j == self.layout.axis:
-                self.exchange(src)
-            dev.sweep_async(j, dt, src, dst, j)
+                self.slow_sweep(dt, src, dst, j)
+            else:
+                dev.sweep_async(j, dt, src, dst, j)
             src = dst
         speeds, nonfinite = dev.fetch(nd)
         red = self.allreduce_max(np.array(list(speeds) + [1.0 if f else 0.0 for f in nonfinite]))
@@ -274,8 +324,9 @@ class Slab:
         for j in range(first_bad + 1):
             dst = sim._scratch[j % 2]
             if j == self.layout.axis:
-                self.exchange(src)
-            dev.sweep_async(j, dt, src, dst, 0, literal=True)
+                self.slow_sweep(dt, src, dst, 0, literal=True)
+            else:
+                dev.sweep_async(j, dt, src, dst, 0, literal=True)
             dev.fetch(1)
             src = dst
         loc = dev.first_nonfinite(src)

@@ -88,6 +88,25 @@ class OracleEngine:
         self.speeds[slot] = max(self.speeds[slot], smax)
         self.flags[slot] = self.flags[slot] or not np.all(np.isfinite(self.bufs[dst][self._isl()]))
 
+    # segment-range launches: the oracle sweeps whole pencils, so ranges are
+    # collected and the sweep runs once all segments of the axis were
+    # requested (interior segments read no ghost row, so running them after
+    # the halo exchange gives the same bytes as the device's early launch)
+    def segments(self, axis):
+        n = self.cells[axis]
+        seg_len = max(4, -(-n // 4))
+        return -(-n // seg_len), seg_len
+
+    def sweep_async_range(self, axis, dt, src, dst, slot, seg_begin, seg_end, literal=False):
+        nseg, _ = self.segments(axis)
+        pend = self.__dict__.setdefault("_pending", {})
+        key = (axis, dt, src, dst, slot)
+        got = pend.setdefault(key, set())
+        got.update(range(seg_begin, seg_end))
+        if len(got) == nseg:
+            del pend[key]
+            self.sweep_async(axis, dt, src, dst, slot, literal)
+
     def fetch(self, n):
         out = (self.speeds[:n], self.flags[:n])
         self.speeds = [0.0] * 4

@@ -445,3 +445,34 @@ def test_device_controller_blowup_location(where):
         res.append((exc.value.state, exc.value.cell, exc.value.step, sim.steps_accepted))
         sim.close()
     assert res[0] == res[1]
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_segment_range_launches_compose_bitwise(dtype):
+    """clb_sweep_async_range: the slow-axis sweep split into interior and
+    edge segment launches (multi-GPU overlap) equals one full launch."""
+    problem = P.get_problem("shallow_water2d")
+    spec = P.GridSpec((70, 203), (-1, -1), (1, 1), 3)
+    g = P.create_grid(spec, np.dtype(dtype))
+    P.fill_initial(g, problem.initial_profile("radial_dam_break", {}, spec))
+    params = problem.make_params({})
+    outs = []
+    for split in (False, True):
+        sim = P.Simulation(g, problem.solver, params,
+                           P.BoundarySpec.uniform(P.BoundaryKind.REFLECTIVE, (1, 2)),
+                           initial_max_speed=problem.speed_bound(g, params))
+        dev = sim.device_grid
+        dev.set_segments(1, 16)
+        nseg, seg_len = dev.segments(1)
+        assert nseg >= 3
+        dev.sweep_async(0, 0.002, 0, 1, 0)
+        if split:
+            dev.sweep_async_range(1, 0.002, 1, 2, 1, 1, nseg - 1)
+            dev.sweep_async_range(1, 0.002, 1, 2, 1, nseg - 1, nseg)
+            dev.sweep_async_range(1, 0.002, 1, 2, 1, 0, 1)
+        else:
+            dev.sweep_async(1, 0.002, 1, 2, 1)
+        speeds, flags = dev.fetch(2)
+        outs.append((dev.download(2).tobytes(), speeds, flags))
+        sim.close()
+    assert outs[0] == outs[1]
