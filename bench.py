@@ -174,19 +174,20 @@ class ClockSampler:
             "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
             "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
         }
-        while not self._stop.is_set():
+        while True:
             try:
-                util = nv.nvmlDeviceGetUtilizationRates(self._h).gpu
+                # every sample of the timed region counts (short regions would
+                # otherwise record nothing: utilisation is a 1/6 s average)
                 mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
-                if util > 0:
-                    self.samples.append(mhz)
+                self.samples.append(mhz)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
                 for k, bit in names.items():
                     if r & bit:
                         self.reasons.add(k)
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            if self._stop.wait(0.02):
+                break
 
     def stop(self):
         self._stop.set()

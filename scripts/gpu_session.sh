@@ -18,8 +18,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --c
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv \
   --log-file $O/launches_sw8192.csv python bench.py --workload sw8192 --steps 4 --warmup 3 --no-cpu > /dev/null 2>&1
 # full capture of the two sweep kernels on the north-star grid
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep -s 12 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel|sweep_contig" -s 6 -c 2 \
   -o $O/prof_sw8192 python bench.py --workload sw8192 --steps 3 --warmup 3 --no-cpu > $O/ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep -s 12 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel|sweep_contig" -s 6 -c 2 \
   -o $O/prof_c2 python bench.py --workload c2 --steps 3 --warmup 3 --no-cpu > $O/ncu_full_c2.log 2>&1
 echo done > $O/DONE
