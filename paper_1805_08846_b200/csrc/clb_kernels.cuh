@@ -652,6 +652,8 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
   constexpr int KC = CarryLayout<T, S>::kCell, KF = CarryLayout<T, S>::kFan;
   constexpr int KA = CarryLayout<T, S>::kAll;
   __shared__ T carry[4][2][KA];
+  // per-warp double buffer of the next chunk's cells (cp.async, no registers)
+  __shared__ T stage[4][2][M][32];
 
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -671,11 +673,34 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
     const int lo = seg * a.seg_len;
     const int hi = min(a.n, lo + a.seg_len);
 
+    // chunk cells stream through shared memory with per-thread async copies,
+    // one chunk ahead; the ghost remap is applied at issue, the reflective
+    // negation at read
+    auto issue = [&](int bb, int buf) {
+      bool neg;
+      const int js = remap(min(bb + lane, hi + 1), a.n, a.bc_lo, a.bc_hi, neg);
+      const T* p = qrow + js;
+#pragma unroll
+      for (int k = 0; k < M; ++k) cp_async<(int)sizeof(T)>(&stage[wib][buf][k][lane], p + k * a.sstride);
+      cp_async_commit();
+    };
+    issue(lo - 2, 0);
+    int cur = 0;
     for (int b = lo - 2; b <= hi + 1; b += 32) {
       const int x = b + lane;
       const bool first = b == lo - 2;
+      if (b + 32 <= hi + 1) {
+        issue(b + 32, cur ^ 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      bool negq;
+      remap(min(x, hi + 1), a.n, a.bc_lo, a.bc_hi, negq);
       T q[M];
-      load_cell<T, M>(qrow, a.sstride, 1, min(x, hi + 1), a, q);
+#pragma unroll
+      for (int k = 0; k < M; ++k) q[k] = neg_if(stage[wib][cur][k][lane], negq && k == a.nv);
+      cur ^= 1;
       Cell c;
       Fan F;
       T G[M], o[M];
