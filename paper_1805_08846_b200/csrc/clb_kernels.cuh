@@ -185,6 +185,9 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
   }
 }
 
+#ifndef CLB_CONTIG_DEPTH
+#define CLB_CONTIG_DEPTH 1
+#endif
 #ifndef CLB_CONTIG_NSTAGE
 #define CLB_CONTIG_NSTAGE 3
 #endif
@@ -653,7 +656,8 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
   constexpr int KA = CarryLayout<T, S>::kAll;
   __shared__ T carry[4][2][KA];
   // per-warp double buffer of the next chunk's cells (cp.async, no registers)
-  __shared__ T stage[4][2][M][32];
+  constexpr int kDepth = CLB_CONTIG_DEPTH;  // chunks in flight ahead of the march
+  __shared__ T stage[4][kDepth + 1][M][32];
 
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -684,23 +688,30 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
       for (int k = 0; k < M; ++k) cp_async<(int)sizeof(T)>(&stage[wib][buf][k][lane], p + k * a.sstride);
       cp_async_commit();
     };
-    issue(lo - 2, 0);
+    // prologue: chunks 0 .. kDepth-1 in flight (empty groups past the end
+    // keep the group count uniform)
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d) {
+      if (lo - 2 + 32 * d <= hi + 1) issue(lo - 2 + 32 * d, d);
+      else cp_async_commit();
+    }
     int cur = 0;
     for (int b = lo - 2; b <= hi + 1; b += 32) {
       const int x = b + lane;
       const bool first = b == lo - 2;
-      if (b + 32 <= hi + 1) {
-        issue(b + 32, cur ^ 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
+      {
+        const int nb = b + 32 * kDepth;
+        const int slot = (cur + kDepth) % (kDepth + 1);
+        if (nb <= hi + 1) issue(nb, slot);
+        else cp_async_commit();
+        cp_async_wait<kDepth>();
       }
       bool negq;
       remap(min(x, hi + 1), a.n, a.bc_lo, a.bc_hi, negq);
       T q[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) q[k] = neg_if(stage[wib][cur][k][lane], negq && k == a.nv);
-      cur ^= 1;
+      cur = cur == kDepth ? 0 : cur + 1;
       Cell c;
       Fan F;
       T G[M], o[M];
