@@ -72,7 +72,7 @@ WORKLOADS = {
 }
 
 
-def build_inputs(name, world=1, rank=0, dist=None, transport="nccl"):
+def build_inputs(name, world=1, rank=0, dist=None, transport="nccl", scale=1):
     """Workload inputs.  world > 1: weak scaling -- the slowest axis grows by
     `world`, each rank owns one slab of the workload's size and fills only its
     own cells (global cell centres, so every byte equals the 1-GPU layout)."""
@@ -80,7 +80,7 @@ def build_inputs(name, world=1, rank=0, dist=None, transport="nccl"):
     from paper_1805_08846_b200.slab import Slab
     prob, cells, lower, upper, profile, options, bc, lim, prec, label = WORKLOADS[name]
     problem = P.get_problem(prob)
-    cells = tuple(cells[:-1]) + (cells[-1] * world,)
+    cells = tuple(cells[:-1]) + (cells[-1] * world * scale,)
     spec = P.GridSpec(cells, lower, upper, problem.num_states)
     bspec = P.BoundarySpec.uniform(P.BoundaryKind(bc), problem.normal_velocity)
     params = problem.make_params({})
@@ -222,7 +222,8 @@ def ncu_traffic(workload, kernel):
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    inp = build_inputs(args.workload)
+    # the same global workload as the B200 arm (weak-scaled x N on the slowest axis)
+    inp = build_inputs(args.workload, scale=world)
     rate, nthreads, steps, el = cpu_rate(inp, max_steps=args.steps, warmup=args.warmup)
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
@@ -230,7 +231,9 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64" if inp["dtype"] == np.float64 else "f32", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": inp["label"], "cells": list(inp["spec"].cells)},
+        "config": {"workload": inp["label"] + (f", weak-scaled x{world} on the slowest axis"
+                                               if world > 1 else ""),
+                   "cells": list(inp["spec"].cells)},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": nthreads, "kind": "port",
                          "sample": f"{steps} steps of the full workload on {nthreads} threads "
                                    "(oracle/clawref.c + oracle/oracle.py controller)"},
@@ -380,8 +383,10 @@ def run_gpu(args, rank, world):
                    "cells": list(inp["spec"].cells),
                    "steps_accepted": acc, "steps_reverted": rev,
                    "l2": "flushed between steps (1 GiB write, untimed; also hides the host launch latency of the step's first sweep)",
-                   "parallelism": (f"slab x{world} along the slowest axis, NCCL halo "
-                                   "exchange + max-allreduce" if world > 1 else "single GPU"),
+                   "parallelism": (f"slab x{world} along the slowest axis, "
+                                   f"{'NCCL' if args.transport == 'nccl' else 'host-staged gloo'} "
+                                   "halo exchange (overlapped with the slow sweep) + max-allreduce"
+                                   if world > 1 else "single GPU"),
                    "vs_baseline_ref": "CUDACLAW SW 1000^2 fp64 9.2 ms/step, C2050 (BASELINE.md)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": f"{kname} (axis {dom})",
