@@ -185,6 +185,12 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
   }
 }
 
+#ifndef CLB_EXACT32
+#define CLB_EXACT32 0
+#endif
+#ifndef CLB_CONTIG_FAST32
+#define CLB_CONTIG_FAST32 0
+#endif
 #ifndef CLB_CONTIG_DEPTH
 #define CLB_CONTIG_DEPTH 1
 #endif
@@ -546,7 +552,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
   T smax = T(0);
   uint32_t fin = 0xffffffffu;
   bool bad = false;
-  if (LIT) {
+  // fp32 shallow water: the exact fp32 division (zero numerators short-cut)
+  // beats the fp64-pipe fast path (8 divisions per cell; y 0.99 vs 1.33 ms at
+  // 8192^2); acoustics' two limiter divisions meet tiny far-field waves that
+  // send div.rn.f32 to its slow path, so it keeps the fast path (1.09 vs 1.35)
+  if (LIT || (sizeof(T) == 4 && (S::NW >= 3 || CLB_EXACT32))) {
     segment_pass<T, S, LIM, LIT, CONTIG, ExactArith>(a, L, maps, smem, full, empty, 0, smax, fin, bad);
   } else {
     segment_pass<T, S, LIM, LIT, CONTIG, FastArith>(a, L, maps, smem, full, empty, 0, smax, fin, bad);
@@ -718,7 +728,7 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
       bool bad = false;
       // fp32: the exact branchy division (zero numerators short-cut) measured
       // faster in this kernel than the fp64-pipe fast path
-      if (LIT || sizeof(T) == 4) {
+      if (LIT || (sizeof(T) == 4 && !CLB_CONTIG_FAST32)) {
         contig_chunk<T, S, LIT, ExactArith>(a, L.dtdx, lim_id, q, first, lane, carry[wib], c, F, G,
                                             o, bad);
       } else {
