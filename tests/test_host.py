@@ -32,6 +32,37 @@ def test_desc_struct_matches_header_layout():
     assert _native.ClbDesc.cells.offset == 24 and _native.ClbDesc.bc.offset == 136
 
 
+def test_abi_structs_match_a_c_compiler(tmp_path):
+    """sizeof/offsetof of every struct the ctypes binding mirrors, as gcc
+    lays them out from include/clawb200.h."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    checks = {
+        "clb_desc": (_native.ClbDesc, ["cells", "spacing", "params", "bc", "normal_velocity"]),
+        "clb_batch": (_native.ClbBatch, ["prev_reverted", "cur", "stop", "max_accepted",
+                                         "n_attempts", "status", "fail_dt"]),
+        "clb_attempt": (_native.ClbAttempt, ["dt_retry", "accepted", "landed"]),
+    }
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "clawb200.h"', "int main(void){"]
+    for st, (_, fields) in checks.items():
+        src.append(f'printf("{st} %zu\\n", sizeof({st}));')
+        for f in fields:
+            src.append(f'printf("{st}.{f} %zu\\n", offsetof({st}, {f}));')
+    src.append("return 0;}")
+    c = tmp_path / "abi.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)], check=True)
+    out = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                       check=True).stdout.splitlines())
+    for st, (cls, fields) in checks.items():
+        assert int(out[st]) == ctypes.sizeof(cls), st
+        for f in fields:
+            assert int(out[f"{st}.{f}"]) == getattr(cls, f).offset, f"{st}.{f}"
+
+
 def test_create_failure_reports_error_without_gpu_or_bad_args():
     d = _native.ClbDesc()
     d.ndim = 4
