@@ -131,9 +131,9 @@ int clb_sweep_async(clb_handle h, int axis, double dt, int src, int dst, int slo
                     int literal);
 int clb_fetch(clb_handle h, int nslots, double *max_abs_speed, int32_t *nonfinite);
 
-/* Segment decomposition of a strided sweep along its axis (nseg segments of
- * seg_len cells; the contiguous x sweep reports one segment), and a launch
- * of segments [seg_begin, seg_end) only.  Segment k reads rows
+/* Segment decomposition of a sweep along its axis (nseg segments of seg_len
+ * cells), and a launch of segments [seg_begin, seg_end) only (strided y/z
+ * sweeps).  Segment k reads rows
  * [k*seg_len - 2, min(n, (k+1)*seg_len) + 2), so the segments that stay
  * clear of the ghost rows can run while a halo exchange is in flight
  * (multi-GPU overlap); results are bitwise those of one full launch. */

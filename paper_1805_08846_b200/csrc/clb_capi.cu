@@ -680,8 +680,8 @@ int clb_sweep_segments(clb_handle h, int axis, int32_t* nseg, int32_t* seg_len) 
   if (!h || !nseg || !seg_len) return fail(h, CLB_EINVAL, "null argument");
   if (axis < 0 || axis >= h->ndim) return fail(h, CLB_EINVAL, "sweep axis out of range");
   const clb::GenericArgs g = sweep_geometry(h, axis, 0, 1);
-  *nseg = g.contig ? 1 : g.nseg;
-  *seg_len = g.contig ? (int32_t)g.n : g.seg_len;
+  *nseg = g.nseg;
+  *seg_len = g.seg_len;
   return CLB_OK;
 }
 
