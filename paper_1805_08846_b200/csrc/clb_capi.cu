@@ -224,6 +224,9 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   }();
   nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, g.n / min_seg));
   int64_t L = (g.n + nseg - 1) / nseg;
+  // warp-marching x sweep: a segment spans L + 4 cells of 32-lane chunks, so
+  // L + 4 is rounded up to a multiple of 32 (no idle lanes in the last chunk)
+  if (axis == 0 && g.contig == 1) L = std::max<int64_t>(28, (L + 4 + 31) / 32 * 32 - 4);
   if (h->seg_override[axis] > 0) L = h->seg_override[axis];
   L = (L + align - 1) / align * align;
   g.seg_len = (int)L;

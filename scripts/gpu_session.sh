@@ -8,7 +8,7 @@ mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt 2>&1
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
-for w in c2 sw8192 sw8192f32 c1 c3 c5 c5f32; do
+for w in c2 sw8192 sw8192hump sw8192f32 c1 c3 c4 c5 c5f32; do
   timeout 400 python bench.py --workload $w --steps 20 --warmup 5 $( [ $w != c2 ] && echo --no-cpu ) > $O/bench_$w.json 2> $O/bench_$w.err
 done
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
