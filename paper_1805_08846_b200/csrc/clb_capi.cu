@@ -57,6 +57,7 @@ struct clb_ctx {
   Result* h_res = nullptr;
   int num_sms = 148;
   int seg_override[3] = {0, 0, 0};
+  int resident[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // [axis][contig mode]: CTAs per SM
   clb::TmaMaps maps;        // per buffer: load map, store map
   // device-resident controller (clb_run_batch)
   clb::DevCtl* d_ctl = nullptr;
@@ -155,6 +156,23 @@ bool make_tensor_map(clb_ctx* h, int buf, bool store, void* out) {
   return r == CUDA_SUCCESS;
 }
 
+cudaError_t dispatch_family(clb_ctx* h, int axis, bool literal, const clb::GenericArgs& g,
+                            cudaStream_t st);
+
+// Resident CTAs per SM of the (non-literal) sweep kernel the geometry selects
+// (cudaOccupancyMaxActiveBlocksPerMultiprocessor, cached per axis and mode).
+int resident_ctas(clb_ctx* h, int axis, const clb::GenericArgs& g0) {
+  int& r = h->resident[axis][g0.contig];
+  if (r == 0) {
+    clb::GenericArgs g = g0;
+    int occ = 0;
+    g.occ_out = &occ;
+    if (dispatch_family(h, axis, false, g, h->stream) != cudaSuccess || occ < 1) occ = 1;
+    r = occ;
+  }
+  return r;
+}
+
 // Geometry of one sweep: which kernel, extents and strides.
 clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   clb::GenericArgs g;
@@ -175,9 +193,9 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   g.num_sms = h->num_sms;
   const int64_t nx = h->cells[0], ny = h->cells[1], nz = h->cells[2];
   // Work decomposition: 128 pencils per CTA; segments along the sweep axis
-  // until ~6 CTAs per SM are in flight, but never shorter than 16 cells (each
-  // segment re-reads 4 cells and re-solves 3 fans of its neighbour;
-  // CLB_MIN_SEG overrides, profiles/r1_notes.md).
+  // (chosen below against the resident CTA slots), never shorter than 16
+  // cells (each segment re-reads 4 cells and re-solves 3 fans of its
+  // neighbour; CLB_MIN_SEG overrides, profiles/r1_notes.md).
   const int64_t target_ctas = (int64_t)h->num_sms * 6;
   int64_t pen_ctas;
   // x-sweep kernel: the TMA tensor-map variant wins when the march is
@@ -217,23 +235,69 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   }
   // contig stages are 48 bytes of a row: segment starts must stay aligned
   const int64_t align = (axis == 0 && g.contig == 2) ? 48 / h->itemsize : 1;
-  int64_t nseg = (target_ctas + pen_ctas - 1) / pen_ctas;
   static const int64_t min_seg = [] {
     const char* e = getenv("CLB_MIN_SEG");
     return e ? std::max<int64_t>(4, atoll(e)) : (int64_t)16;
   }();
-  nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, g.n / min_seg));
-  int64_t L = (g.n + nseg - 1) / nseg;
-  // warp-marching x sweep: a segment spans L + 4 cells of 32-lane chunks, so
-  // L + 4 is rounded up to a multiple of 32 (no idle lanes in the last chunk)
-  if (axis == 0 && g.contig == 1) L = std::max<int64_t>(28, (L + 4 + 31) / 32 * 32 - 4);
-  if (h->seg_override[axis] > 0) L = h->seg_override[axis];
-  L = (L + align - 1) / align * align;
+  // segment length L of a candidate segment count: warp-marching spans L + 4
+  // cells in 32-lane chunks, so L + 4 is a multiple of 32 (no idle lanes)
+  auto seg_len_of = [&](int64_t ns) {
+    int64_t L = (g.n + ns - 1) / ns;
+    if (axis == 0 && g.contig == 1) L = std::max<int64_t>(28, (L + 4 + 31) / 32 * 32 - 4);
+    return (L + align - 1) / align * align;
+  };
+  // CTAs a segment count launches (the warp-march packs 4 row-warps per CTA)
+  auto ctas_of = [&](int64_t ns) {
+    return (axis == 0 && g.contig == 1) ? (ny * nz * ns + 3) / 4 : pen_ctas * ns;
+  };
+  // Segment count: maximise (busy fraction of the last wave) x (L / (L+4),
+  // the share of non-redundant work) over the resident CTA slots, so that
+  // grids do not end on a nearly empty wave (8192^2: 896 CTAs on 296 slots
+  // left 140 SMs idle for a quarter of the sweep).
+  (void)target_ctas;
+  const int64_t slots = (int64_t)h->num_sms * resident_ctas(h, axis, g);
+  const int64_t max_seg = std::max<int64_t>(1, std::min<int64_t>(g.n / min_seg, 4096));
+  int64_t best_n = 1;
+  double best_e = -1.0;
+  for (int64_t ns = 1; ns <= max_seg; ++ns) {
+    const int64_t L = seg_len_of(ns);
+    const int64_t ns2 = (g.n + L - 1) / L;
+    if (ns2 != ns) continue;
+    const int64_t c = ctas_of(ns2);
+    const int64_t waves = (c + slots - 1) / slots;
+    const double e = (double)c / (double)(waves * slots) * ((double)L / (double)(L + 4));
+    if (e > best_e + 1e-9) {
+      best_e = e;
+      best_n = ns2;
+    }
+  }
+  int64_t L = seg_len_of(best_n);
+  if (h->seg_override[axis] > 0) L = (h->seg_override[axis] + align - 1) / align * align;
   g.seg_len = (int)L;
   g.nseg = (int)((g.n + L - 1) / L);
   g.seg_begin = 0;
   g.seg_end = g.nseg;
   return g;
+}
+
+cudaError_t dispatch_family(clb_ctx* h, int axis, bool literal, const clb::GenericArgs& g,
+                            cudaStream_t st) {
+  const bool d64 = h->itemsize == 8;
+  const int nd = h->ndim;
+  switch (h->d.solver_id) {
+    case CLB_SOLVER_ACOUSTICS:
+      return d64 ? clb::launch_acoustics_f64(nd, axis, literal, g, st)
+                 : clb::launch_acoustics_f32(nd, axis, literal, g, st);
+    case CLB_SOLVER_SHALLOW_WATER:
+      return d64 ? clb::launch_shallow_water_f64(nd, axis, literal, g, st)
+                 : clb::launch_shallow_water_f32(nd, axis, literal, g, st);
+    case CLB_SOLVER_ADVECTION:
+      return d64 ? clb::launch_advection_f64(nd, axis, literal, g, st)
+                 : clb::launch_advection_f32(nd, axis, literal, g, st);
+    default:
+      return d64 ? clb::launch_vc_acoustics_f64(nd, axis, literal, g, st)
+                 : clb::launch_vc_acoustics_f32(nd, axis, literal, g, st);
+  }
 }
 
 // indirect: buffers and dt are read by the kernel from h->d_ctl (batch graphs)
@@ -265,28 +329,7 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
     tl.b = take_event(h);
     cudaEventRecord(tl.a, h->stream);
   }
-  cudaError_t e;
-  const bool d64 = h->itemsize == 8;
-  const int nd = h->ndim;
-  cudaStream_t st = h->stream;
-  switch (h->d.solver_id) {
-    case CLB_SOLVER_ACOUSTICS:
-      e = d64 ? clb::launch_acoustics_f64(nd, axis, literal, g, st)
-              : clb::launch_acoustics_f32(nd, axis, literal, g, st);
-      break;
-    case CLB_SOLVER_SHALLOW_WATER:
-      e = d64 ? clb::launch_shallow_water_f64(nd, axis, literal, g, st)
-              : clb::launch_shallow_water_f32(nd, axis, literal, g, st);
-      break;
-    case CLB_SOLVER_ADVECTION:
-      e = d64 ? clb::launch_advection_f64(nd, axis, literal, g, st)
-              : clb::launch_advection_f32(nd, axis, literal, g, st);
-      break;
-    default:
-      e = d64 ? clb::launch_vc_acoustics_f64(nd, axis, literal, g, st)
-              : clb::launch_vc_acoustics_f32(nd, axis, literal, g, st);
-      break;
-  }
+  cudaError_t e = dispatch_family(h, axis, literal, g, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "sweep launch");
   if (h->timing && !indirect) {
     cudaEventRecord(tl.b, h->stream);

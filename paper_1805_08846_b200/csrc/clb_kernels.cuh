@@ -813,6 +813,7 @@ struct GenericArgs {
   int seg_len, nseg;
   int seg_begin, seg_end;  // segment range of this launch (strided kernels)
   int num_sms;
+  int* occ_out;            // non-null: report resident CTAs per SM instead of launching
 };
 
 template <typename T>
@@ -840,6 +841,9 @@ inline SweepArgs<T> to_args(const GenericArgs& g) {
 
 template <typename T, class S, int LIM, bool LIT>
 inline cudaError_t launch_contig_shfl(const GenericArgs& g, cudaStream_t st) {
+  if (g.occ_out)
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(g.occ_out, sweep_contig<T, S, LIM, LIT>,
+                                                         128, 0);
   SweepArgs<T> a = to_args<T>(g);
   const int64_t warps = (int64_t)g.n1 * g.n2 * g.nseg;
   const int64_t blocks = (warps + 3) / 4;
@@ -858,6 +862,8 @@ inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  if (g.occ_out) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(g.occ_out, fn, kThreads,
+                                                                      Geo::SMEM);
   SweepArgs<T> a = to_args<T>(g);
   static const TmaMaps none{};
   dim3 grid((unsigned)((g.n1 + kConsumers - 1) / kConsumers), (unsigned)(g.seg_end - g.seg_begin),
