@@ -195,10 +195,10 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #define CLB_CONTIG_DEPTH 1
 #endif
 #ifndef CLB_CONTIG_NSTAGE
-#define CLB_CONTIG_NSTAGE 3
+#define CLB_CONTIG_NSTAGE 2
 #endif
 #ifndef CLB_SW_MINB
-#define CLB_SW_MINB 2
+#define CLB_SW_MINB 3
 #endif
 // Resident CTAs per SM the register allocation is sized for: the fp64
 // shallow-water march needs ~150 registers (2 CTAs), everything else fits 3.
