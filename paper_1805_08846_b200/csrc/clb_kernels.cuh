@@ -197,13 +197,19 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #ifndef CLB_CONTIG_NSTAGE
 #define CLB_CONTIG_NSTAGE 2
 #endif
+#ifndef CLB_F32_MINB
+#define CLB_F32_MINB 4
+#endif
+#ifndef CLB_F64_MINB
+#define CLB_F64_MINB 3
+#endif
 #ifndef CLB_SW_MINB
 #define CLB_SW_MINB 3
 #endif
 // Resident CTAs per SM the register allocation is sized for: the fp64
 // shallow-water march needs ~150 registers (2 CTAs), everything else fits 3.
 template <typename T, class S> constexpr int kMinBlocks() {
-  return (sizeof(T) == 8 && S::NW >= 3) ? CLB_SW_MINB : (sizeof(T) == 4 ? 4 : 3);
+  return (sizeof(T) == 8 && S::NW >= 3) ? CLB_SW_MINB : (sizeof(T) == 4 ? CLB_F32_MINB : CLB_F64_MINB);
 }
 
 template <typename T, class S, bool CONTIG> struct StageGeom {
