@@ -209,7 +209,7 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   // and run faster warp-marching (56 vs 69 us, profiles/r1_notes.md).
   const int64_t ncells = h->cells[0] * h->cells[1] * h->cells[2];
   const int contig_mode = contig_env ? contig_env
-                          : ((h->d.solver_id == CLB_SOLVER_SHALLOW_WATER && h->itemsize == 8 &&
+                          : ((h->d.solver_id == CLB_SOLVER_SHALLOW_WATER &&
                               ncells >= ((int64_t)1 << 22)) ? 2 : 1);
   if (axis == 0) {
     g.contig = (contig_mode == 2 && h->have_maps) ? 2 : 1;
