@@ -197,6 +197,9 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #ifndef CLB_CONTIG_NSTAGE
 #define CLB_CONTIG_NSTAGE 2
 #endif
+#ifndef CLB_STRIDED_NC
+#define CLB_STRIDED_NC 3   // rows per strided stage (a multiple of 3)
+#endif
 #ifndef CLB_F32_MINB
 #define CLB_F32_MINB 4
 #endif
@@ -213,7 +216,7 @@ template <typename T, class S> constexpr int kMinBlocks() {
 }
 
 template <typename T, class S, bool CONTIG> struct StageGeom {
-  static constexpr int NC = CONTIG ? (kRowStrideContig / (int)sizeof(T)) : 3;  // cells/stage
+  static constexpr int NC = CONTIG ? (kRowStrideContig / (int)sizeof(T)) : CLB_STRIDED_NC;  // cells/stage
   static constexpr int BYTES = CONTIG ? S::M * kConsumers * kRowStrideContig
                                       : S::M * NC * kConsumers * (int)sizeof(T);
   // two leading alignment dummies: the prologue cells sit at r = 2..5, so every
