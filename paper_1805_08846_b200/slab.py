@@ -210,7 +210,7 @@ class Slab:
         if self.transport == "nccl":
             return self._exchange_nccl(sides, m)
         self._exchange_host(sides, m)
-        return None
+        return ((), None)   # completed; the split slow sweep still runs (same path as NCCL)
 
     @staticmethod
     def exchange_end(pending) -> None:
