@@ -326,6 +326,9 @@ def run_gpu(args, rank, world):
     peak, peak_kind = measured_peaks()
     kname = "x-sweep (contiguous axis)" if dom == 0 else f"axis-{dom} sweep (strided, TMA ring)"
     traffic = ncu_traffic(args.workload, f"axis{dom}")
+    ws = 3 * bytes_per_launch / 2   # state + 2 scratch buffers
+    l2_note = (f"working set ({ws / 1e6:.0f} MB, state + 2 scratch buffers) fits the 126 MB L2: "
+               "the sweeps are latency-bound, not HBM-bound" if ws < 126e6 else None)
     sim.close()
 
     # e2e through the public API with pinned host buffers
@@ -398,6 +401,7 @@ def run_gpu(args, rank, world):
                      "method": "CUDA events recorded on the launch stream around every "
                                "sweep launch of the timed region (clb_enable_timing)",
                      "per_axis_ms_in_step": per_axis,
+                     "note": l2_note,
                      "kernel_share_of_step": sum(ms_axis[:ndim]) / max(total_ms_local, 1e-9)},
         "cpu_baseline": cpu,
         "e2e": e2e,
