@@ -700,8 +700,12 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
     // one chunk ahead; the ghost remap is applied at issue, the reflective
     // negation at read
     auto issue = [&](int bb, int buf) {
-      bool neg;
-      const int js = remap(min(bb + lane, hi + 1), a.n, a.bc_lo, a.bc_hi, neg);
+      // chunks clear of both ends need no ghost remap (warp-uniform test)
+      int js = min(bb + lane, hi + 1);
+      if (!(bb >= 0 && bb + 31 < a.n)) {
+        bool neg;
+        js = remap(js, a.n, a.bc_lo, a.bc_hi, neg);
+      }
       const T* p = qrow + js;
 #pragma unroll
       for (int k = 0; k < M; ++k) cp_async<(int)sizeof(T)>(&stage[wib][buf][k][lane], p + k * a.sstride);
@@ -725,8 +729,8 @@ __global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
         else cp_async_commit();
         cp_async_wait<kDepth>();
       }
-      bool negq;
-      remap(min(x, hi + 1), a.n, a.bc_lo, a.bc_hi, negq);
+      bool negq = false;
+      if (!(b >= 0 && b + 31 < a.n)) remap(min(x, hi + 1), a.n, a.bc_lo, a.bc_hi, negq);
       T q[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) q[k] = neg_if(stage[wib][cur][k][lane], negq && k == a.nv);
