@@ -80,6 +80,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Bulk async copy shared -> global (SASS UBLKCP), bulk_group completion.
+// dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // TMA tensor copies (SASS UTMALDG / UTMASTG).  The 4-D tensor maps are built
 // on the host by cuTensorMapEncodeTiled (csrc/clb_capi.cu make_tensor_map).

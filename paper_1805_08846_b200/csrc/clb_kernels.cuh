@@ -197,6 +197,9 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #ifndef CLB_CONTIG_NSTAGE
 #define CLB_CONTIG_NSTAGE 2
 #endif
+#ifndef CLB_STRIDED_OUT
+#define CLB_STRIDED_OUT 2  // strided sweeps stage outputs for row bulk stores (0: per-thread stores)
+#endif
 #ifndef CLB_STRIDED_NC
 #define CLB_STRIDED_NC 3   // rows per strided stage (a multiple of 3)
 #endif
@@ -223,9 +226,14 @@ template <typename T, class S, bool CONTIG> struct StageGeom {
   // 3-cell group starts on ring phase 0, and every contig stage box starts
   // 16-byte aligned (TMA requirement) because segments start at multiples of NC.
   static constexpr int A = 2;
-  static constexpr int NSTAGE_RAW = CONTIG ? (S::M >= 4 ? 2 : CLB_CONTIG_NSTAGE) : (72 * 1024 / BYTES);
+  // output staging tiles: TMA stores (contig); row bulk stores for the
+  // compute-bound fp64 shallow-water strided sweeps (y 1.88 -> 1.69 ms at
+  // 8192^2), per-thread stores elsewhere (acoustics y/z, which need the
+  // deeper input ring: 1.45 vs 1.64 ms with staging; fp32 SW 0.83 vs 0.96)
+  static constexpr int NOUT = CONTIG ? 2 : ((S::NW >= 3 && sizeof(T) == 8) ? CLB_STRIDED_OUT : 0);
+  static constexpr int NSTAGE_RAW =
+      CONTIG ? (S::M >= 4 ? 2 : CLB_CONTIG_NSTAGE) : (72 * 1024 / BYTES - NOUT);
   static constexpr int NSTAGE = NSTAGE_RAW < 2 ? 2 : (NSTAGE_RAW > 6 ? 6 : NSTAGE_RAW);
-  static constexpr int NOUT = CONTIG ? 2 : 0;  // output staging tiles (TMA store)
   static constexpr int SMEM = (NSTAGE + NOUT) * BYTES + 2 * NSTAGE * 8;
   static_assert(A % 3 == 2, "prologue phase");
 };
@@ -365,7 +373,10 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   }
   const bool halo_lo = a.bc_lo == BC_HALO, halo_hi = a.bc_hi == BC_HALO;
   const bool refl_lo = a.bc_lo == BC_REFLECTIVE, refl_hi = a.bc_hi == BC_REFLECTIVE;
-  unsigned char* outs = smem + NSTAGE * G::BYTES;  // contig output tiles
+  unsigned char* outs = smem + NSTAGE * G::BYTES;  // output tiles
+  // strided output rows go out as bulk copies when a row's bytes are a
+  // multiple of 16 (a partial last column block may not be)
+  const bool bulk_out = !CONTIG && ((nvalid * (int)sizeof(T)) & 15) == 0;
 
   // Ghost cells (boundary.py:87-122) are fixed up in the stage itself, once
   // per stage that holds any, by the thread owning the row/column, so the
@@ -433,6 +444,15 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 #pragma unroll
         for (int q = 0; q < M; ++q) mr.fin = min(mr.fin, finite_key(o[q]));
       }
+    } else if (G::NOUT > 0 && bulk_out) {
+      const int e = r - A - 4;
+      T* ob = reinterpret_cast<T*>(outs + ((e / NC) & 1) * G::BYTES);
+#pragma unroll
+      for (int q = 0; q < M; ++q) ob[(q * NC + e % NC) * kConsumers + t] = o[q];
+      if (valid && active) {
+#pragma unroll
+        for (int q = 0; q < M; ++q) mr.fin = min(mr.fin, finite_key(o[q]));
+      }
     } else if (valid && active) {
       T* dst = pout + (int64_t)(lo + r - A - 4) * a.astride;
 #pragma unroll
@@ -454,11 +474,25 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
     named_barrier_sync(1, kConsumers);
     if (t == 0) {
       const unsigned char* ob = outs + (tile & 1) * G::BYTES;
-      const int cx = a.tx0 + lo + tile * NC;
-      const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
+      if (CONTIG) {
+        const int cx = a.tx0 + lo + tile * NC;
+        const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
 #pragma unroll
-      for (int q = 0; q < M; ++q)
-        tma_store_4d(map_st, ob + q * kConsumers * kRowStrideContig, cx, cy, cz, q);
+        for (int q = 0; q < M; ++q)
+          tma_store_4d(map_st, ob + q * kConsumers * kRowStrideContig, cx, cy, cz, q);
+      } else {
+        // strided: each output row of the tile is nvalid contiguous cells
+        const uint32_t rowbytes = (uint32_t)nvalid * (uint32_t)sizeof(T);
+        T* base = L.qout + pb + (int64_t)blockIdx.z * a.t2stride;
+        for (int c = 0; c < NC; ++c) {
+          const int e = tile * NC + c;
+          if (lo + e >= hi) break;
+#pragma unroll
+          for (int q = 0; q < M; ++q)
+            bulk_s2g(base + (int64_t)(lo + e) * a.astride + q * a.sstride,
+                     ob + ((q * NC + c) * kConsumers) * (int)sizeof(T), rowbytes);
+        }
+      }
       bulk_commit();
     }
     flushed = tile;
@@ -492,7 +526,8 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
         mr.template step<2>(q, a, v && active, o);
         emit(r0 + 2, v, o);
         // the group's last cell closes an output tile every NC cells
-        if (CONTIG && (r0 + 2 - A - 4) % NC == NC - 1) flush((r0 + 2 - A - 4) / NC);
+        if ((CONTIG || (G::NOUT > 0 && bulk_out)) && (r0 + 2 - A - 4) % NC == NC - 1)
+          flush((r0 + 2 - A - 4) / NC);
       } else if (r0 == A + 1) {
         fetch(st, c0, q);
         mr.template fan<0>(q, a, active);          // F(lo-1)
@@ -508,7 +543,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-  if (CONTIG) {
+  if (CONTIG || (G::NOUT > 0 && bulk_out)) {
     const int last = (ncell - 1 - A - 4) / NC;  // tile of the segment's last cell
     if (last > flushed) flush(last);
     if (t == 0) bulk_wait<0>();
