@@ -212,8 +212,9 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #ifndef CLB_SW_MINB
 #define CLB_SW_MINB 3
 #endif
-// Resident CTAs per SM the register allocation is sized for: the fp64
-// shallow-water march needs ~150 registers (2 CTAs), everything else fits 3.
+// Resident CTAs per SM the register allocation is sized for: fp64 shallow
+// water 3 (128 registers; the march would take ~168 at 2 CTAs, but the extra
+// warps win, profiles/r1_notes.md), other fp64 3, fp32 4.
 template <typename T, class S> constexpr int kMinBlocks() {
   return (sizeof(T) == 8 && S::NW >= 3) ? CLB_SW_MINB : (sizeof(T) == 4 ? CLB_F32_MINB : CLB_F64_MINB);
 }
