@@ -212,11 +212,15 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #ifndef CLB_SW_MINB
 #define CLB_SW_MINB 3
 #endif
+#ifndef CLB_SW_MINB_STRIDED
+#define CLB_SW_MINB_STRIDED CLB_SW_MINB
+#endif
 // Resident CTAs per SM the register allocation is sized for: fp64 shallow
 // water 3 (128 registers; the march would take ~168 at 2 CTAs, but the extra
 // warps win, profiles/r1_notes.md), other fp64 3, fp32 4.
-template <typename T, class S> constexpr int kMinBlocks() {
-  return (sizeof(T) == 8 && S::NW >= 3) ? CLB_SW_MINB : (sizeof(T) == 4 ? CLB_F32_MINB : CLB_F64_MINB);
+template <typename T, class S, bool CONTIG> constexpr int kMinBlocks() {
+  return (sizeof(T) == 8 && S::NW >= 3) ? (CONTIG ? CLB_SW_MINB : CLB_SW_MINB_STRIDED)
+                                        : (sizeof(T) == 4 ? CLB_F32_MINB : CLB_F64_MINB);
 }
 
 template <typename T, class S, bool CONTIG> struct StageGeom {
@@ -575,7 +579,7 @@ __device__ __forceinline__ int segment_stages(const SweepArgs<T>& a) {
 // same TMA-issuing thread after bulk_wait), and its (smax, fin) replace pass
 // 1's.  Literal (blow-up) kernels run one ExactArith pass.
 template <typename T, class S, int LIM, bool LIT, bool CONTIG>
-__global__ void __launch_bounds__(kThreads, kMinBlocks<T, S>())
+__global__ void __launch_bounds__(kThreads, kMinBlocks<T, S, CONTIG>())
     sweep_kernel(const SweepArgs<T> a, const __grid_constant__ TmaMaps maps) {
   Live<T> L;
   if (!resolve_live(a, L)) return;
