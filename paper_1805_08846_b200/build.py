@@ -24,7 +24,8 @@ SOURCES = [("clb_capi.cu", [], "clb_capi.o")] + [
     for fam in ("acoustics", "shallow_water", "advection", "vc_acoustics")
     for isz in (4, 8)
 ]
-HEADERS = ["clb_solvers.cuh", "clb_kernels.cuh", "clb_async.cuh", "../../include/clawb200.h"]
+HEADERS = ["clb_solvers.cuh", "clb_kernels.cuh", "clb_async.cuh", "clb_controller.cuh",
+           "../../include/clawb200.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

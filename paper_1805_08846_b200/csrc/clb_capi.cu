@@ -31,11 +31,7 @@ namespace {
 
 thread_local std::string g_create_error;
 
-struct Result {
-  unsigned long long smax[4];
-  int nonfinite[4];
-  unsigned long long first_bad;
-};
+using clb::Result;
 
 struct TimedLaunch {
   int axis;
@@ -302,7 +298,7 @@ cudaError_t dispatch_family(clb_ctx* h, int axis, bool literal, const clb::Gener
 
 // indirect: buffers and dt are read by the kernel from h->d_ctl (batch graphs)
 int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bool literal,
-                 bool indirect = false, int seg_begin = 0, int seg_end = -1) {
+                 bool indirect = false, int seg_begin = 0, int seg_end = -1, bool fuse = false) {
   if (axis < 0 || axis >= h->ndim) return fail(h, CLB_EINVAL, "sweep axis out of range");
   if (src < 0 || src > 2 || dst < 0 || dst > 2) return fail(h, CLB_EINVAL, "buffer index out of range");
   if (src == dst) return fail(h, CLB_EINVAL, "sweep cannot run in place");
@@ -310,6 +306,8 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
   if (slot < 0 || slot > 3) return fail(h, CLB_EINVAL, "result slot out of range");
   clb::GenericArgs g = sweep_geometry(h, axis, src, dst);
   g.ctl = indirect ? h->d_ctl : nullptr;
+  g.fuse_ctl = (indirect && fuse) ? 1 : 0;
+  g.res = h->d_res;
   if (seg_end >= 0) {
     if (g.contig) return fail(h, CLB_EINVAL, "segment ranges apply to strided sweeps only");
     if (seg_begin < 0 || seg_end > g.nseg || seg_begin >= seg_end)
@@ -400,106 +398,10 @@ __global__ void selftest_arith_kernel(const double* a, const double* b, int64_t 
 }
 
 
-// ---------------------------------------------------------------------------
-// Device-resident controller (clb_run_batch): timestep.py:151-243 in fp64 on
-// one device thread.  Every expression keeps the reference's operation order
-// (explicit __d*_rn so nothing is contracted); Python's min(a, b) / max(a, b)
-// are "b if b < a else a" / "b if b > a else a".
-
-// estimate_dt (timestep.py:151-177) + the run_until loop guards
-// (timestep.py:263-270) for the next attempt, or end the batch.
-__device__ void ctl_prepare_next(clb::DevCtl* c) {
-  if (c->done) return;
-  if (c->max_accepted >= 0 && c->n_accepted >= c->max_accepted) {
-    c->status = CLB_BATCH_MAXSTEPS; c->done = 1; return;
-  }
-  if (!(c->t < c->stop)) { c->status = CLB_BATCH_STOP; c->done = 1; return; }
-  if (c->n_attempts >= c->log_cap) { c->status = CLB_BATCH_LOGFULL; c->done = 1; return; }
-  const double s = c->last_max_speed;
-  double dt;
-  if (s > 0.0) {
-    dt = __ddiv_rn(__dmul_rn(c->cfl_target, c->min_spacing), s);
-    dt = c->dt_cap < dt ? c->dt_cap : dt;
-  } else {
-    dt = c->dt_cap;
-  }
-  int landed = 0;
-  const double remaining = __dsub_rn(c->stop, c->t);
-  if (dt >= remaining) {
-    dt = remaining;
-    landed = 1;
-  }
-  if (!isfinite(dt)) { c->status = CLB_BATCH_DTERR; c->done = 1; return; }
-  c->dt = dt;
-  c->landed = landed;
-  // timestep.py:200-206: sweep j reads the previous output, writes scratch[j % 2]
-  int cur = c->cur;
-  for (int j = 0; j < c->ndim; ++j) {
-    const int dst = (j % 2 == 0) ? c->s0 : c->s1;
-    c->src[j] = cur;
-    c->dst[j] = dst;
-    cur = dst;
-  }
-}
-
-__global__ void ctl_prepare(clb::DevCtl* c) { ctl_prepare_next(c); }
-
-// The attempt's verdict (timestep.py:207-243), then the next attempt.
-__global__ void ctl_finish(clb::DevCtl* c, Result* r) {
-  if (c->done) return;
-  double step_speed = 0.0;
-  for (int j = 0; j < c->ndim; ++j) {
-    if (r->nonfinite[j]) {
-      c->status = CLB_BATCH_BLOWUP;
-      c->fail_sweep = j;
-      c->done = 1;
-      return;
-    }
-    const double sj = __longlong_as_double((long long)r->smax[j]);
-    step_speed = sj > step_speed ? sj : step_speed;
-  }
-  for (int j = 0; j < 4; ++j) { r->smax[j] = 0ull; r->nonfinite[j] = 0; }
-  const double nu = __ddiv_rn(__dmul_rn(c->dt, step_speed), c->min_spacing);
-  const bool accepted = nu <= c->cfl_max;
-  clb_attempt rec;
-  rec.t_start = c->t;
-  rec.dt = c->dt;
-  rec.max_speed = step_speed;
-  rec.nu = nu;
-  rec.dt_retry = __longlong_as_double(0x7ff8000000000000ll);  // None
-  rec.accepted = accepted ? 1 : 0;
-  rec.landed = (c->landed && accepted) ? 1 : 0;
-  clb_attempt* log = (clb_attempt*)c->log;
-  if (accepted) {
-    const int last = (c->ndim - 1) % 2;
-    const int fin = last == 0 ? c->s0 : c->s1;
-    const int other = last == 0 ? c->s1 : c->s0;
-    c->s0 = c->cur;
-    c->s1 = other;
-    c->cur = fin;
-    c->t = c->landed ? c->stop : __dadd_rn(c->t, c->dt);
-    c->n_accepted += 1;
-    c->nu_max = nu > c->nu_max ? nu : c->nu_max;
-    c->prev_reverted = 0;
-  } else {
-    rec.dt_retry = __ddiv_rn(__dmul_rn(c->cfl_target, c->min_spacing), step_speed);
-    if (c->prev_reverted && nu >= c->prev_nu) {
-      // UnstableStepError: logged (the reference counts the revert first),
-      // prev_nu kept for the message, last_max_speed not updated
-      log[c->n_attempts] = rec;
-      c->n_attempts += 1;
-      c->status = CLB_BATCH_UNSTABLE;
-      c->done = 1;
-      return;
-    }
-    c->prev_reverted = 1;
-    c->prev_nu = nu;
-  }
-  c->last_max_speed = step_speed;
-  log[c->n_attempts] = rec;
-  c->n_attempts += 1;
-  ctl_prepare_next(c);
-}
+namespace clb {
+__global__ void ctl_prepare(DevCtl* c) { ctl_prepare_next(c); }
+__global__ void ctl_finish(DevCtl* c, Result* r) { ctl_finish_dev(c, r); }
+}  // namespace clb
 
 extern "C" {
 
@@ -994,9 +896,18 @@ int build_batch_graph(clb_ctx* h) {
   }
   CLB_CUDA(h, cudaStreamSynchronize(h->stream));
   CLB_CUDA(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  // one-thread controller kernel per attempt; CLB_FUSED_CTL=1 folds it into
+  // the last CTA of the attempt's final sweep instead, which measured slower
+  // (C2 e2e 6.73 vs 7.15, C1 1.91 vs 2.11 Gcell-upd/s: the per-CTA fence and
+  // counter and the serial tail cost more than the saved graph node)
+  static const bool fused = [] {
+    const char* e = getenv("CLB_FUSED_CTL");
+    return e && e[0] == '1';
+  }();
   int r = 0;
-  for (int j = 0; j < h->ndim && !r; ++j) r = launch_sweep(h, j, 1.0, 0, 1, j, false, true);
-  if (!r) ctl_finish<<<1, 1, 0, h->stream>>>(h->d_ctl, h->d_res);
+  for (int j = 0; j < h->ndim && !r; ++j)
+    r = launch_sweep(h, j, 1.0, 0, 1, j, false, true, 0, -1, fused && j == h->ndim - 1);
+  if (!r && !fused) clb::ctl_finish<<<1, 1, 0, h->stream>>>(h->d_ctl, h->d_res);
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(h->stream, &g);
   if (r) { if (g) cudaGraphDestroy(g); return r; }
@@ -1056,7 +967,7 @@ extern "C" int clb_run_batch(clb_handle h, clb_batch* b, clb_attempt* log, int64
   CLB_CUDA(h, cudaMemcpyAsync(h->d_ctl, h->h_ctl, sizeof(clb::DevCtl), cudaMemcpyHostToDevice,
                               h->stream));
   CLB_CUDA(h, cudaMemsetAsync(h->d_res, 0, sizeof(Result), h->stream));
-  ctl_prepare<<<1, 1, 0, h->stream>>>(h->d_ctl);
+  clb::ctl_prepare<<<1, 1, 0, h->stream>>>(h->d_ctl);
   CLB_CUDA(h, cudaGetLastError());
   // Replay attempts in chunks; the host only polls the done flag between
   // chunks (attempts replayed past the end are no-ops).  A step budget sizes

@@ -57,7 +57,12 @@ struct DevCtl {
   int src[3], dst[3];        // buffer roles of the current attempt's sweeps
   int done, status, fail_sweep, ndim;
   void* log;                 // clb_attempt[log_cap]
+  unsigned int blocks_done;  // CTAs of the fused final sweep that finished
 };
+
+}  // namespace clb
+#include "clb_controller.cuh"
+namespace clb {
 
 template <typename T> struct SweepArgs {
   const T* qin;     // element (0,0,0) of state 0 (interior origin)
@@ -84,6 +89,10 @@ template <typename T> struct SweepArgs {
   int axis;
   double spacing;
   const void* bufs[3];
+  // the attempt's last sweep: its last CTA runs the controller (no separate
+  // controller launch per attempt)
+  int fuse_ctl;
+  Result* res;
 };
 
 // TMA descriptors of the three buffers (load: full padded extent; store:
@@ -182,6 +191,19 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
     const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
     if (bits > *((volatile unsigned long long*)a.smax_bits)) atomicMax(a.smax_bits, bits);
     if (fin == 0u) atomicOr(a.nonfinite, 1);
+    if (a.fuse_ctl) {
+      // last CTA of the attempt's final sweep: every CTA's atomics above are
+      // visible (fence + counter), so it evaluates the attempt and prepares
+      // the next one exactly as the ctl_finish kernel would
+      DevCtl* c = const_cast<DevCtl*>(a.ctl);
+      __threadfence();
+      const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+      if (atomicAdd(&c->blocks_done, 1u) == total - 1u) {
+        __threadfence();
+        c->blocks_done = 0u;
+        ctl_finish_dev(c, a.res);
+      }
+    }
   }
 }
 
@@ -867,6 +889,8 @@ struct GenericArgs {
   int seg_begin, seg_end;  // segment range of this launch (strided kernels)
   int num_sms;
   int* occ_out;            // non-null: report resident CTAs per SM instead of launching
+  int fuse_ctl;
+  Result* res;
 };
 
 template <typename T>
@@ -889,6 +913,8 @@ inline SweepArgs<T> to_args(const GenericArgs& g) {
   a.axis = g.axis;
   a.spacing = g.spacing;
   for (int i = 0; i < 3; ++i) a.bufs[i] = g.bufs[i];
+  a.fuse_ctl = g.fuse_ctl;
+  a.res = g.res;
   return a;
 }
 
