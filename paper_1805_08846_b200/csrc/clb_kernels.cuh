@@ -219,6 +219,9 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #ifndef CLB_CONTIG_NSTAGE
 #define CLB_CONTIG_NSTAGE 2
 #endif
+#ifndef CLB_CONTIG_MINB
+#define CLB_CONTIG_MINB 1  // resident 128-thread CTAs the warp-march register budget targets
+#endif
 #ifndef CLB_STRIDED_OUT
 #define CLB_STRIDED_OUT 2  // strided sweeps stage outputs for row bulk stores (0: per-thread stores)
 #endif
@@ -726,7 +729,7 @@ __device__ __forceinline__ void contig_chunk(
 // ---------------------------------------------------------------------------
 // Axis 0 (contiguous): warp-marching kernel.
 template <typename T, class S, int LIM, bool LIT>
-__global__ void __launch_bounds__(128) sweep_contig(const SweepArgs<T> a) {
+__global__ void __launch_bounds__(128, CLB_CONTIG_MINB) sweep_contig(const SweepArgs<T> a) {
   Live<T> L;
   if (!resolve_live(a, L)) return;
   const int lim_id = LIM >= 0 ? LIM : a.lim_id;
