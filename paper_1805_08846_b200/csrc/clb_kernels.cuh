@@ -219,6 +219,9 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #ifndef CLB_CONTIG_NSTAGE
 #define CLB_CONTIG_NSTAGE 2
 #endif
+#ifndef CLB_NO_REDO
+#define CLB_NO_REDO 0
+#endif
 #ifndef CLB_CONTIG_MINB
 #define CLB_CONTIG_MINB 1  // resident 128-thread CTAs the warp-march register budget targets
 #endif
@@ -634,7 +637,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S, CONTIG>())
     segment_pass<T, S, LIM, LIT, CONTIG, ExactArith>(a, L, maps, smem, full, empty, 0, smax, fin, bad);
   } else {
     segment_pass<T, S, LIM, LIT, CONTIG, FastArith>(a, L, maps, smem, full, empty, 0, smax, fin, bad);
-    if (__syncthreads_or(bad)) {
+    // CLB_NO_REDO: timing experiments only (results may differ from div.rn)
+    if (__syncthreads_or(bad) && !CLB_NO_REDO) {
       smax = T(0);
       fin = 0xffffffffu;
       const int k0 = segment_stages<T, S, CONTIG>(a);
