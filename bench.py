@@ -1,9 +1,13 @@
 """Benchmark of the time-step hot path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4]
+                    [--scaling strong|weak] [--impl reference]
 
 One JSON line on rank 0.  A "step" is one ``Simulation.attempt_step`` (all
-ndim fused sweeps + the fp64 CFL controller) over the workload's grid.
+ndim fused sweeps + the fp64 CFL controller) over the workload's grid.  The
+default workload is C4 (BASELINE.json configs[3]: 2-D shallow water
+16384^2, fp64), strong-scaled over N GPUs; ``--workload c5`` (512^3
+acoustics per GPU) weak-scales.
 
 * ``value``: cell-updates/s with the state resident in HBM, each step timed
   with CUDA events on the launch stream (host controller gaps included),
@@ -17,9 +21,11 @@ ndim fused sweeps + the fp64 CFL controller) over the workload's grid.
   (m states read + m written per cell) / its mean CUDA-event
   duration, against MEASURED_PEAKS.json ``hbm_gbs``.
 * ``cpu_baseline``: the oracle (C restatement of the reference path, all host
-  threads) on a bounded sample of the same workload.
+  threads) on a bounded sample of the same workload: the middle band of the
+  global grid holding about 2^24 cells.
 * ``--impl reference``: the reference's CPU path (oracle port) timed on the
-  host cores on this workload; rank 0 only.
+  host cores, rank 0 only, each step one attempt over that same band; the
+  line's ``config`` is identical to the B200 arm's.
 """
 
 from __future__ import annotations
@@ -56,7 +62,7 @@ WORKLOADS = {
            "C3: 3D acoustics 256^3 two-material medium, superbee, fp64"),
     "c4": ("shallow_water2d", (16384, 16384), (-1, -1), (1, 1), "radial_dam_break", {},
            "reflective", "mc", "double",
-           "C4: 2D shallow water 16384x16384 radial dam-break (1 GPU), fp64"),
+           "C4: 2D shallow water 16384x16384 radial dam-break, reflective, MC, adaptive CFL dt, fp64"),
     "c5": ("acoustics3d", (512, 512, 512), (0, 0, 0), (1, 1, 1), "gaussian_pressure",
            {"width": 0.1}, "periodic", "mc", "double",
            "C5: 3D acoustics 512^3 per GPU, MC, periodic, fp64"),
@@ -75,21 +81,62 @@ WORKLOADS = {
 }
 
 
-def build_inputs(name, world=1, rank=0, dist=None, transport="nccl", scale=1):
-    """Workload inputs.  world > 1: weak scaling -- the slowest axis grows by
-    `world`, each rank owns one slab of the workload's size and fills only its
-    own cells (global cell centres, so every byte equals the 1-GPU layout)."""
+#: default scaling mode per workload (BASELINE.json: C4 strong, C5 weak)
+DEFAULT_SCALING = {"c4": "strong"}
+#: cells of the bounded CPU sample (one band of the workload's grid)
+CPU_SAMPLE_CELLS = 1 << 24
+
+
+def global_cells(name, world, scaling):
+    """Global grid of the run: weak scaling grows the slowest axis by `world`
+    (each rank keeps the workload's size), strong scaling splits the
+    workload's own grid over the ranks."""
+    cells = WORKLOADS[name][1]
+    if scaling == "weak":
+        return tuple(cells[:-1]) + (cells[-1] * world,)
+    return tuple(cells)
+
+
+def config_of(args, world, scaling):
+    """The run's `config`, identical in both arms (same_config)."""
+    prob, cells, lower, upper, profile, options, bc, lim, prec, label = WORKLOADS[args.workload]
+    gcells = global_cells(args.workload, world, scaling)
+    return {
+        "workload": label,
+        "name": args.workload,
+        "cells": list(gcells),
+        "scaling": scaling,
+        "parallelism": (f"slab x{world} along the slowest axis, NCCL halo exchange "
+                        "(overlapped with the slow sweep) + max-allreduce" if world > 1
+                        else "single GPU"),
+        "l2": "flushed between steps (1 GiB write, untimed); the grid is larger than L2"
+              if int(np.prod(gcells)) * 8 > 126e6 else
+              "flushed between steps (1 GiB write, untimed); the working set fits L2",
+        "step": "one Simulation.attempt_step (all ndim fused sweeps + the fp64 CFL "
+                "controller); Gcell-updates counts accepted steps only",
+    }
+
+
+def build_inputs(name, gcells, world=1, rank=0, dist=None, transport="nccl", band=None):
+    """Workload inputs on the global grid `gcells`.  world > 1: this rank's
+    slab (global cell centres, so every byte equals the 1-GPU layout).
+    band=(index, count): one slab of the global grid, alone (the bounded CPU
+    sample), with the workload's physical boundaries on its faces."""
     import paper_1805_08846_b200 as P
     from paper_1805_08846_b200.slab import Slab
-    prob, cells, lower, upper, profile, options, bc, lim, prec, label = WORKLOADS[name]
+    prob, _, lower, upper, profile, options, bc, lim, prec, label = WORKLOADS[name]
     problem = P.get_problem(prob)
-    cells = tuple(cells[:-1]) + (cells[-1] * world * scale,)
-    spec = P.GridSpec(cells, lower, upper, problem.num_states)
+    spec = P.GridSpec(tuple(gcells), lower, upper, problem.num_states)
     bspec = P.BoundarySpec.uniform(P.BoundaryKind(bc), problem.normal_velocity)
     params = problem.make_params({})
     prof = problem.initial_profile(profile, dict(options), spec)
     slab = None
-    if world > 1:
+    if band is not None:
+        part = Slab(spec, bspec, band[0], band[1], None)
+        grid = P.create_grid(part.local_spec, P.grid.DTYPES[prec])
+        part.fill_initial(grid, prof)
+        speed = problem.speed_bound(grid, params)
+    elif world > 1:
         slab = Slab(spec, bspec, rank, world, dist, transport=transport)
         grid = P.create_grid(slab.local_spec, P.grid.DTYPES[prec])
         slab.fill_initial(grid, prof)
@@ -101,6 +148,20 @@ def build_inputs(name, world=1, rank=0, dist=None, transport="nccl", scale=1):
     return dict(P=P, problem=problem, spec=spec, grid=grid, params=params, speed=speed,
                 bspec=bspec, limiter=P.LimiterKind(lim), label=label, dtype=grid.dtype,
                 slab=slab, local_cells=grid.spec.num_cells)
+
+
+def cpu_sample_inputs(name, gcells):
+    """The bounded CPU sample: the middle band of the global grid holding
+    about CPU_SAMPLE_CELLS cells (the whole grid if it is smaller)."""
+    n = int(np.prod(gcells))
+    parts = max(1, min(gcells[-1] // 2, n // CPU_SAMPLE_CELLS))
+    if parts == 1:
+        return build_inputs(name, gcells), "the whole grid"
+    inp = build_inputs(name, gcells, band=(parts // 2, parts))
+    c = inp["grid"].spec.cells
+    return inp, (f"the middle {c[-1]}-{'row' if len(c) == 2 else 'plane'} band "
+                 f"({'x'.join(map(str, c))} cells) of the {'x'.join(map(str, gcells))} grid, "
+                 "same profile and boundary kinds")
 
 
 # ---------------------------------------------------------------------------
@@ -122,12 +183,13 @@ def oracle_from_inputs(inp, nthreads):
 
 
 def cpu_rate(inp, budget_s=12.0, max_steps=None, warmup=1):
-    """Oracle throughput on all host threads (bounded sample)."""
+    """Oracle throughput on all host threads: `warmup` untimed attempts, then
+    `max_steps` attempts (or as many as fit `budget_s`)."""
     nthreads = os.cpu_count() or 1
     sim = oracle_from_inputs(inp, nthreads)
     for _ in range(warmup):
         sim.attempt_step()
-    cells = inp["spec"].num_cells
+    cells = inp["grid"].spec.num_cells
     acc0 = sim.steps_accepted
     t0 = time.perf_counter()
     steps = 0
@@ -222,24 +284,26 @@ def ncu_traffic(workload, kernel):
         return None
 
 
-def run_reference(args, rank, world):
+def run_reference(args, rank, world, scaling):
+    """The reference arm: the reference's CPU path (oracle port) on the host
+    cores, rank 0 only, each step one attempt over the bounded sample of this
+    run's global workload."""
     if rank != 0:
         return 0
-    # the same global workload as the B200 arm (weak-scaled x N on the slowest axis)
-    inp = build_inputs(args.workload, scale=world)
+    gcells = global_cells(args.workload, world, scaling)
+    inp, sample = cpu_sample_inputs(args.workload, gcells)
     rate, nthreads, steps, el = cpu_rate(inp, max_steps=args.steps, warmup=args.warmup)
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * el / max(steps, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
         "dtype": "f64" if inp["dtype"] == np.float64 else "f32", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": inp["label"] + (f", weak-scaled x{world} on the slowest axis"
-                                               if world > 1 else ""),
-                   "cells": list(inp["spec"].cells)},
+        "config": config_of(args, world, scaling),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": nthreads, "kind": "port",
-                         "sample": f"{steps} steps of the full workload on {nthreads} threads "
-                                   "(oracle/clawref.c + oracle/oracle.py controller)"},
+                         "sample": f"each step: one attempt_step over {sample}; {steps} timed "
+                                   f"steps after {args.warmup} warm-up on {nthreads} threads "
+                                   "(oracle/clawref.c sweeps + oracle/oracle.py controller)"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -250,7 +314,7 @@ def flush_l2(buf):
     buf.zero_()
 
 
-def run_gpu(args, rank, world):
+def run_gpu(args, rank, world, scaling):
     import torch
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
@@ -264,7 +328,8 @@ def run_gpu(args, rank, world):
         else:
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
-    inp = build_inputs(args.workload, world, rank, dist, args.transport)
+    gcells = global_cells(args.workload, world, scaling)
+    inp = build_inputs(args.workload, gcells, world, rank, dist, args.transport)
     P = inp["P"]
     sim = P.Simulation(inp["grid"], inp["problem"].solver, inp["params"], inp["bspec"],
                        limiter=inp["limiter"], initial_max_speed=inp["speed"], device=local,
@@ -294,6 +359,9 @@ def run_gpu(args, rank, world):
     acc0, rev0 = sim.steps_accepted, sim.steps_reverted
     for _ in range(args.steps):
         flush_l2(flush)
+        # the device idles before the step starts: the first sweep's launch
+        # latency is inside the timed region
+        stream.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -318,18 +386,19 @@ def run_gpu(args, rank, world):
         total_ms = float(t.item())
     value = cells * acc / (total_ms / 1e3) / 1e9
 
-    # roofline: dominant kernel (largest total time)
+    # roofline: dominant kernel (largest time per launch)
     dom = max(range(ndim), key=lambda a: per_axis[a])
     bytes_per_launch = lcells * m * 2 * isz
     mean_ms = per_axis[dom]
     achieved = bytes_per_launch / (mean_ms / 1e3) / 1e9
     peak, peak_kind = measured_peaks()
-    kname = "x-sweep (contiguous axis)" if dom == 0 else f"axis-{dom} sweep (strided, TMA ring)"
+    xvar = dev.x_variant() if hasattr(dev, "x_variant") else None
+    kname = (("x-sweep (contiguous axis, " + ("TMA tensor-map transpose" if xvar == 2
+                                               else "warp-march") + ")") if dom == 0
+             else f"axis-{dom} sweep (strided, bulk-copy ring)")
     traffic = ncu_traffic(args.workload, f"axis{dom}")
-    ws = 3 * bytes_per_launch / 2   # state + 2 scratch buffers
-    l2_note = (f"working set ({ws / 1e6:.0f} MB, state + 2 scratch buffers) fits the 126 MB L2: "
-               "the sweeps are latency-bound, not HBM-bound" if ws < 126e6 else None)
     sim.close()
+    del flush
 
     # e2e through the public API with pinned host buffers
     from paper_1805_08846_b200._native import PinnedBuffer
@@ -354,6 +423,8 @@ def run_gpu(args, rank, world):
     e2e_acc = rep.steps_accepted
     e2e_att = len(rep.attempts)
     sim2.close()
+    pin_in.free()
+    pin_out.free()
     if dist:
         t = torch.tensor([e2e_s], device=rdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -363,9 +434,11 @@ def run_gpu(args, rank, world):
     e2e = {"value": cells * e2e_acc / e2e_s / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": int(state_bytes / args.steps),
            "d2h_bytes_per_step": int(state_bytes / args.steps + rec_bytes * e2e_att / args.steps),
-           "api": "Simulation.run_until(max_steps=K) (device-resident controller, one batch): "
-                  "pinned H2D upload of the state, K steps, D2H of the state and the K "
-                  "attempt records",
+           "api": "Simulation.run_until(max_steps=K)"
+                  + (" (device-resident controller, one batch)" if world == 1 else
+                     " (per-attempt host loop with NCCL halo exchange + max-allreduce)")
+                  + ": pinned H2D upload of the state, K steps, D2H of the state and the "
+                    "attempt records; wall clock, max over ranks",
            "steps_accepted": e2e_acc, "attempts": e2e_att}
 
     if rank != 0:
@@ -374,34 +447,30 @@ def run_gpu(args, rank, world):
         return 0
     cpu = None
     if world == 1 and not args.no_cpu:
-        rate, nthreads, steps, el = cpu_rate(inp, budget_s=args.cpu_budget)
+        del inp["grid"]
+        sinp, sample = cpu_sample_inputs(args.workload, gcells)
+        rate, nthreads, steps, el = cpu_rate(sinp, budget_s=args.cpu_budget)
         cpu = {"value": rate, "unit": UNIT, "cores": nthreads, "kind": "port",
-               "sample": f"{steps} steps of the same {inp['label'].split(':')[0]} grid in "
-                         f"{el:.1f} s on {nthreads} host threads (oracle/clawref.c)"}
+               "sample": f"{steps} attempt_steps over {sample} in {el:.1f} s on {nthreads} "
+                         "host threads (oracle/clawref.c)"}
     is_sw64 = inp["problem"].solver_name == "shallow_water" and inp["dtype"] == np.float64
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": (value / PUBLISHED_SW_FP64) if is_sw64 else None,
+        "scaling": scaling, "vs_baseline": (value / PUBLISHED_SW_FP64) if is_sw64 else None,
         "dtype": "f64" if inp["dtype"] == np.float64 else "f32", "data": "synthetic",
-        "config": {"workload": inp["label"] + (f", weak-scaled x{world} on the slowest axis"
-                                               if world > 1 else ""),
-                   "cells": list(inp["spec"].cells),
-                   "steps_accepted": acc, "steps_reverted": rev,
-                   "l2": "flushed between steps (1 GiB write, untimed; also hides the host launch latency of the step's first sweep)",
-                   "parallelism": (f"slab x{world} along the slowest axis, "
-                                   f"{'NCCL' if args.transport == 'nccl' else 'host-staged gloo'} "
-                                   "halo exchange (overlapped with the slow sweep) + max-allreduce"
-                                   if world > 1 else "single GPU"),
-                   "vs_baseline_ref": "CUDACLAW SW 1000^2 fp64 9.2 ms/step, C2050 (BASELINE.md)"},
+        "config": config_of(args, world, scaling),
+        "run": {"steps_accepted": acc, "steps_reverted": rev,
+                "vs_baseline_ref": "CUDACLAW SW 1000^2 fp64 9.2 ms/step, C2050 (BASELINE.md)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": f"{kname} (axis {dom})",
                      "bytes_per_launch": bytes_per_launch, "mean_launch_ms": mean_ms,
                      "peak_kind": peak_kind,
+                     "algorithmic_bytes": "m states read + m written per cell per sweep "
+                                          f"({m} x 2 x {isz} B) x {lcells} cells per launch",
                      "method": "CUDA events recorded on the launch stream around every "
                                "sweep launch of the timed region (clb_enable_timing)",
                      "per_axis_ms_in_step": per_axis,
-                     "note": l2_note,
                      "kernel_share_of_step": sum(ms_axis[:ndim]) / max(total_ms_local, 1e-9)},
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -419,19 +488,23 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", choices=["strong", "weak"], default=None,
+                    help="strong: the workload's grid split over the ranks; weak: each rank "
+                         "owns one workload-sized slab (default: strong for c4, else weak)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
                     help="halo transport for N>1 (host: gloo, for ranks sharing one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    scaling = args.scaling or DEFAULT_SCALING.get(args.workload, "weak")
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
-        return run_reference(args, rank, world)
-    return run_gpu(args, rank, world)
+        return run_reference(args, rank, world, scaling)
+    return run_gpu(args, rank, world, scaling)
 
 
 if __name__ == "__main__":

@@ -101,6 +101,18 @@ int clb_set_stream(clb_handle h, void *cuda_stream);
  * recompute their shared fans, sweep.py:11-16); exposed for tests/tuning. */
 int clb_set_segments(clb_handle h, int axis, int seg_len);
 
+/* x-sweep (contiguous axis) kernel variant of this handle:
+ *   CLB_XVAR_AUTO  (0) by solver and grid size (the measured best),
+ *   CLB_XVAR_MARCH (1) warp-marching kernel (one lane per cell, shuffles),
+ *   CLB_XVAR_TMA   (2) TMA tensor-map transpose kernel (one thread per row).
+ * Results are bitwise independent of the variant; exposed so every variant
+ * can be held to the oracle at any size (tests) and for tuning.  The
+ * process-wide default is CLB_CONTIG=tma|shfl (read once), else AUTO. */
+enum { CLB_XVAR_AUTO = 0, CLB_XVAR_MARCH = 1, CLB_XVAR_TMA = 2 };
+int clb_set_x_variant(clb_handle h, int variant);
+/* The variant the next x sweep of this handle launches (1 or 2). */
+int clb_x_variant(clb_handle h, int32_t *variant);
+
 /* Interior transfer, frame-payload order: state-major, then z, y, x (x
  * fastest), ghost cells excluded; nbytes must equal m*prod(cells)*itemsize.
  * buf in {0,1,2}. */

@@ -35,8 +35,11 @@ EXPORTS = (
     "clb_attempt_step", "clb_first_nonfinite", "clb_halo_layout", "clb_halo_copy", "clb_solve_pairs",
     "clb_enable_timing", "clb_timing", "clb_host_alloc", "clb_host_free", "clb_memory_info",
     "clb_selftest_arith", "clb_run_batch", "clb_frame_size", "clb_write_frame",
-    "clb_sweep_segments", "clb_sweep_async_range",
+    "clb_sweep_segments", "clb_sweep_async_range", "clb_set_x_variant", "clb_x_variant",
 )
+
+#: x-sweep kernel variants (clb_set_x_variant)
+XVAR_AUTO, XVAR_MARCH, XVAR_TMA = 0, 1, 2
 
 #: clb_run_batch statuses (include/clawb200.h)
 BATCH_STOP, BATCH_MAXSTEPS, BATCH_LOGFULL, BATCH_BLOWUP, BATCH_UNSTABLE, BATCH_DTERR = range(6)
@@ -109,6 +112,8 @@ def lib():
         "clb_version": (_int, []),
         "clb_set_stream": (_int, [_vp, _vp]),
         "clb_set_segments": (_int, [_vp, _int, _int]),
+        "clb_set_x_variant": (_int, [_vp, _int]),
+        "clb_x_variant": (_int, [_vp, ctypes.POINTER(_i32)]),
         "clb_upload": (_int, [_vp, _int, _vp, _sz]),
         "clb_download": (_int, [_vp, _int, _vp, _sz]),
         "clb_upload_padded": (_int, [_vp, _int, _vp, _sz]),
@@ -244,6 +249,16 @@ class DeviceGrid:
 
     def set_segments(self, axis: int, seg_len: int):
         _check(lib().clb_set_segments(self.handle, axis, seg_len), self.handle)
+
+    def set_x_variant(self, variant: int):
+        """x-sweep kernel: XVAR_AUTO, XVAR_MARCH (warp-march) or XVAR_TMA."""
+        _check(lib().clb_set_x_variant(self.handle, int(variant)), self.handle)
+
+    def x_variant(self) -> int:
+        """The kernel variant the next x sweep launches (XVAR_MARCH / XVAR_TMA)."""
+        v = _i32(0)
+        _check(lib().clb_x_variant(self.handle, ctypes.byref(v)), self.handle)
+        return int(v.value)
 
     def set_stream(self, stream_ptr: int | None):
         _check(lib().clb_set_stream(self.handle, stream_ptr or None), self.handle)

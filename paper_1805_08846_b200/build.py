@@ -52,9 +52,23 @@ def build(verbose: bool = False, force: bool = False, variant: str | None = None
           defines: tuple = ()) -> str:
     """Compile and link the library; `variant` + `defines` build a tuning
     variant libclawb200_<variant>.so from its own object directory."""
+    if defines and not variant:
+        # knobs (some timing-only and not bit-exact) never go into the default
+        # library: its objects' staleness check looks at mtimes, not defines
+        raise ValueError("build(defines=...) needs a variant name (libclawb200_<variant>.so)")
     out = OUT if not variant else os.path.join(HERE, f"libclawb200_{variant}.so")
     bdir = BUILD if not variant else os.path.join(CSRC, f"build_{variant}")
-    extra_d = [f"-D{d}" for d in defines]
+    extra_d = [f"-D{d}" for d in defines] if variant else ["-DCLB_DEFAULT_LIB=1"]
+    if variant:
+        # a variant's objects are rebuilt whenever its define set changes
+        os.makedirs(bdir, exist_ok=True)
+        stamp = os.path.join(bdir, "defines.txt")
+        want = "\n".join(sorted(extra_d))
+        old = open(stamp).read() if os.path.exists(stamp) else None
+        if old != want:
+            force = True
+            with open(stamp, "w") as fh:
+                fh.write(want)
     os.makedirs(bdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS]
     objs = []

@@ -53,6 +53,7 @@ struct clb_ctx {
   Result* h_res = nullptr;
   int num_sms = 148;
   int seg_override[3] = {0, 0, 0};
+  int x_variant = 0;        // CLB_XVAR_*: 0 = automatic
   int resident[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // [axis][contig mode]: CTAs per SM
   clb::TmaMaps maps;        // per buffer: load map, store map
   // device-resident controller (clb_run_batch)
@@ -196,15 +197,11 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   int64_t pen_ctas;
   // x-sweep kernel: the TMA tensor-map variant wins when the march is
   // compute-heavy (fp64 shallow water, profiles/r1_notes.md); the warp-shuffle
-  // variant wins elsewhere.  CLB_CONTIG=tma|shfl overrides.
-  static const int contig_env = [] {
-    const char* e = getenv("CLB_CONTIG");
-    return e ? (e[0] == 't' ? 2 : 1) : 0;
-  }();
-  // Small grids (C2, 1024^2) have too few 128-row blocks for the TMA variant
-  // and run faster warp-marching (56 vs 69 us, profiles/r1_notes.md).
+  // variant wins elsewhere.  Small grids (C2, 1024^2) have too few 128-row
+  // blocks for the TMA variant and run faster warp-marching (56 vs 69 us).
+  // clb_set_x_variant (per handle) overrides.
   const int64_t ncells = h->cells[0] * h->cells[1] * h->cells[2];
-  const int contig_mode = contig_env ? contig_env
+  const int contig_mode = h->x_variant ? h->x_variant
                           : ((h->d.solver_id == CLB_SOLVER_SHALLOW_WATER &&
                               ncells >= ((int64_t)1 << 22)) ? 2 : 1);
   if (axis == 0) {
@@ -304,6 +301,7 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
   if (src == dst) return fail(h, CLB_EINVAL, "sweep cannot run in place");
   if (!(dt > 0.0)) return fail(h, CLB_EINVAL, "dt must be positive");
   if (slot < 0 || slot > 3) return fail(h, CLB_EINVAL, "result slot out of range");
+  cudaSetDevice(h->d.device);  // handles on several devices in one process
   clb::GenericArgs g = sweep_geometry(h, axis, src, dst);
   g.ctl = indirect ? h->d_ctl : nullptr;
   g.fuse_ctl = (indirect && fuse) ? 1 : 0;
@@ -447,6 +445,11 @@ int clb_create(const clb_desc* desc, clb_handle* out) {
   h->ndim = d.ndim;
   h->M = d.num_states;
   h->itemsize = d.itemsize;
+  {
+    // process-wide default of clb_set_x_variant: CLB_CONTIG=tma|shfl
+    const char* e = getenv("CLB_CONTIG");
+    h->x_variant = e ? (e[0] == 't' ? CLB_XVAR_TMA : CLB_XVAR_MARCH) : CLB_XVAR_AUTO;
+  }
   for (int ax = 0; ax < d.ndim; ++ax) h->cells[ax] = d.cells[ax];
   const int64_t align = 128 / d.itemsize;
   h->xoff = align;
@@ -518,13 +521,34 @@ int clb_set_stream(clb_handle h, void* s) {
   return CLB_OK;
 }
 
-int clb_set_segments(clb_handle h, int axis, int seg_len) {
-  if (!h || axis < 0 || axis > 2 || seg_len < 0) return fail(h, CLB_EINVAL, "bad segment override");
-  h->seg_override[axis] = seg_len;
+static void drop_batch_graph(clb_ctx* h) {
   if (h->batch_exec) cudaGraphExecDestroy(h->batch_exec);
   if (h->batch_graph) cudaGraphDestroy(h->batch_graph);
   h->batch_exec = nullptr;
   h->batch_graph = nullptr;
+}
+
+int clb_set_segments(clb_handle h, int axis, int seg_len) {
+  if (!h || axis < 0 || axis > 2 || seg_len < 0) return fail(h, CLB_EINVAL, "bad segment override");
+  h->seg_override[axis] = seg_len;
+  drop_batch_graph(h);
+  return CLB_OK;
+}
+
+int clb_set_x_variant(clb_handle h, int variant) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  if (variant < CLB_XVAR_AUTO || variant > CLB_XVAR_TMA) return fail(h, CLB_EINVAL, "unknown x-sweep variant");
+  if (variant == CLB_XVAR_TMA && !h->have_maps)
+    return fail(h, CLB_EUNSUPPORTED, "TMA tensor maps unavailable on this device");
+  h->x_variant = variant;
+  drop_batch_graph(h);
+  return CLB_OK;
+}
+
+int clb_x_variant(clb_handle h, int32_t* variant) {
+  if (!h || !variant) return fail(h, CLB_EINVAL, "null argument");
+  const clb::GenericArgs g = sweep_geometry(h, 0, 0, 1);
+  *variant = g.contig;
   return CLB_OK;
 }
 

@@ -29,6 +29,8 @@
 // neighbour exactly as the reference's tiles do (sweep.py:11-16), so results
 // are bitwise independent of the segmentation.
 #pragma once
+#include <atomic>
+
 #include "clb_async.cuh"
 #include "clb_solvers.cuh"
 
@@ -941,12 +943,17 @@ template <typename T, class S, int LIM, bool LIT, bool CONTIG>
 inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
   if (CONTIG && g.contig == 1) return launch_contig_shfl<T, S, LIM, LIT>(g, st);
   using Geo = StageGeom<T, S, CONTIG>;
-  static bool configured = false;
+  // the dynamic shared-memory opt-in is per device: one bit per device
+  // ordinal, set once (atomically: service threads may launch concurrently)
+  static std::atomic<unsigned long long> configured{0ull};
   auto fn = sweep_kernel<T, S, LIM, LIT, CONTIG>;
-  if (!configured) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.fetch_or(bit, std::memory_order_release);
   }
   if (g.occ_out) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(g.occ_out, fn, kThreads,
                                                                       Geo::SMEM);

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import paper_1805_08846_b200 as P
-from paper_1805_08846_b200._native import DeviceGrid
+from paper_1805_08846_b200._native import XVAR_AUTO, XVAR_MARCH, XVAR_TMA, DeviceGrid
 from oracle import oracle as O
 
 import cases
@@ -27,7 +27,9 @@ def _grid_from_padded(qin, c):
     return g
 
 
-def test_golden_sweeps_bitwise(golden_sweeps):
+@pytest.mark.parametrize("variant", [XVAR_AUTO, XVAR_MARCH, XVAR_TMA],
+                         ids=["auto", "x-march", "x-tma"])
+def test_golden_sweeps_bitwise(golden_sweeps, variant):
     meta, arrays = golden_sweeps
     bad = []
     for i, c in enumerate(meta):
@@ -43,14 +45,14 @@ def test_golden_sweeps_bitwise(golden_sweeps):
         }[c["solver"]](c["params"])
         dt = float.fromhex(c["dt_hex"])
         # exact reference spacing: run with dt scaled so dt/dx matches bitwise
-        res = _sweep_exact(grid, out, c, dt, solver, params)
+        res = _sweep_exact(grid, out, c, dt, solver, params, variant)
         exp = arrays[f"qout_{i}"]
         if out.interior().tobytes() != exp.tobytes() or res != float.fromhex(c["smax_hex"]):
             bad.append((i, c["solver"], c["dtype"], c["limiter"], c["bc"], c["axis"]))
     assert not bad, f"{len(bad)}/{len(meta)} mismatching sweeps, first: {bad[:6]}"
 
 
-def _sweep_exact(grid, out, c, dt, solver, params):
+def _sweep_exact(grid, out, c, dt, solver, params, variant=XVAR_AUTO):
     """sweep_axis with the golden case's exact fp64 spacing."""
     nd = len(c["cells"])
     g = DeviceGrid(ndim=nd, cells=tuple(c["cells"]), spacing=tuple(c["spacing"]),
@@ -60,6 +62,7 @@ def _sweep_exact(grid, out, c, dt, solver, params):
                    params=solver.pack_params(params, grid.dtype), bc=[(3, 3)] * nd,
                    normal_velocity=[None] * nd)
     try:
+        g.set_x_variant(variant)
         g.upload_padded(0, grid.data)
         smax, _ = g.sweep(c["axis"], dt, 0, 1)
         out.interior()[...] = g.download(1)
@@ -146,20 +149,25 @@ def _recipe(problem, cells, profile, options, dtype, bc, limiter, steps):
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 @pytest.mark.parametrize("bc", ["outflow", "reflective", "periodic"])
 @pytest.mark.parametrize("limiter", ["mc", "superbee", "minmod", "vanleer", "none"])
-def test_random_configs_match_oracle(shape, dtype, bc, limiter):
+@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA], ids=["x-march", "x-tma"])
+def test_random_configs_match_oracle(shape, dtype, bc, limiter, variant):
+    """Both x-sweep kernels (forced per handle) on every shape / BC / limiter."""
     problem, cells, profile, options = shape
     r = _recipe(problem, cells, profile, options, dtype, bc, limiter, steps=4)
     osim, _ = cases.oracle_sim(r)
     oatt = cases.drive(osim, r)
     sim, _ = cases.product_sim(r)
     with sim:
+        sim.device_grid.set_x_variant(variant)
+        assert sim.device_grid.x_variant() == variant
         att = cases.drive(sim, r)
         assert cases.attempts_hex(att) == cases.attempts_hex(oatt)
         assert sim.grid.interior().tobytes() == O.interior(osim.grid).tobytes()
 
 
+@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA], ids=["x-march", "x-tma"])
 @pytest.mark.parametrize("seg", [(1, 1), (7, 5), (33, 40), (64, 3), (1000, 1000)])
-def test_segmentation_is_bitwise_invisible(seg):
+def test_segmentation_is_bitwise_invisible(seg, variant):
     r = _recipe("shallow_water2d", (150, 130), "radial_dam_break", {}, "float64", "reflective",
                 "mc", 3)
     ref_sim, _ = cases.product_sim(r)
@@ -168,6 +176,7 @@ def test_segmentation_is_bitwise_invisible(seg):
         ref = ref_sim.grid.interior().copy()
     sim, _ = cases.product_sim(r)
     with sim:
+        sim.device_grid.set_x_variant(variant)
         sim.device_grid.set_segments(0, seg[0])
         sim.device_grid.set_segments(1, seg[1])
         cases.drive(sim, r)
@@ -341,9 +350,10 @@ def test_fast_division_and_sqrt_are_bitwise_ieee(rng):
     assert min(dfall, sfall, fdfall, fsfall) > 0
 
 
+@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA], ids=["x-march", "x-tma"])
 @pytest.mark.parametrize("limiter", ["mc", "vanleer", "superbee"])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
-def test_slow_path_inputs_match_oracle(rng, limiter, dtype):
+def test_slow_path_inputs_match_oracle(rng, limiter, dtype, variant):
     """Shallow-water sweeps over states that push divisions and square roots
     outside their fast-path domain (subnormal and 1e-300-scale momenta, tiny
     depth jumps, exact zeros): the per-step exact recomputation must keep
@@ -360,10 +370,17 @@ def test_slow_path_inputs_match_oracle(rng, limiter, dtype):
     scale = rng.choice(scales, size=(2, 45, 67))
     g.interior()[1:] = mom * scale
     P.apply_boundary(g, P.BoundarySpec.uniform(P.BoundaryKind.REFLECTIVE, (1, 2)))
+    from paper_1805_08846_b200 import sweep as SW
+    op = SW._operator(spec, np.dtype(dtype), P.get_solver("shallow_water"),
+                      P.LimiterKind(limiter), P.ShallowWaterParams(1.0))
+    op.set_x_variant(variant)
     for axis in (0, 1):
         out = P.create_grid(spec, dtype)
-        res = P.sweep_axis(g, out, axis, 0.004, P.get_solver("shallow_water"),
-                           P.LimiterKind(limiter), P.ShallowWaterParams(1.0))
+        try:
+            res = P.sweep_axis(g, out, axis, 0.004, P.get_solver("shallow_water"),
+                               P.LimiterKind(limiter), P.ShallowWaterParams(1.0))
+        finally:
+            op.set_x_variant(XVAR_AUTO)
         ref = np.zeros_like(g.data)
         smax = O.sweep(g.data.copy(), ref, axis, 0.004, spec.spacing, "shallow_water", limiter,
                        {"gravity": 1.0})

@@ -83,3 +83,15 @@ def test_failed_step_is_409(client):
     r = client.post(f"/sessions/{sid}/evolve", json={"t_target": 0.05})
     assert r.status_code == 409 and "non-finite" in r.json()["detail"]
     client.delete(f"/sessions/{sid}")
+
+
+def test_device_fault_at_create_is_503_not_422(client, monkeypatch):
+    # a CUDA failure while allocating the session is not invalid input
+    from paper_1805_08846_b200 import service as S
+
+    def boom(cfg, device=0):
+        raise P.DeviceError("device allocation failed: out of memory")
+
+    monkeypatch.setattr(S, "build_simulation", boom)
+    r = client.post("/sessions", json={"config_text": CFG})
+    assert r.status_code == 503 and "out of memory" in r.json()["detail"]
