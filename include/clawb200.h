@@ -239,9 +239,12 @@ int clb_run_batch(clb_handle h, clb_batch *b, clb_attempt *log, int64_t log_cap)
  * quotients where the fast path claimed validity but differs bitwise from
  * div.rn, out[1] = same for sqrt(a[i]), out[2] / out[3] = how many
  * quotients / roots fell back to the exact path; out[4..7] the same for the
- * fp32 path on the low 32 bits of a[i], b[i] read as floats.  No handle
- * needed. */
-int clb_selftest_arith(int device, int64_t n, const double *a, const double *b, int64_t out[8]);
+ * fp32 path on the low 32 bits of a[i], b[i] read as floats; out[8] /
+ * out[9] mismatches / fallbacks of the limiter-ratio division (kChkLim: a
+ * zero quotient's sign is free), out[10] / out[11] the same for the Roe
+ * division (kChkNumNormDen) on the pairs with b in [2^-485, 2^513].  No
+ * handle needed. */
+int clb_selftest_arith(int device, int64_t n, const double *a, const double *b, int64_t out[12]);
 
 /* Kernel timing (CUDA events on the launch stream) for the bench: when
  * enabled, every sweep launch is bracketed by events; clb_timing returns

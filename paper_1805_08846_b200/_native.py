@@ -379,14 +379,16 @@ class DeviceGrid:
 def selftest_arith(a, b, device: int = 0):
     """Branch-free div/sqrt of the sweep kernels vs div.rn/sqrt.rn on the
     device: (div mismatches, sqrt mismatches, div fallbacks, sqrt fallbacks)
-    for fp64, then the same four for fp32 (low words of a, b as floats)."""
+    for fp64, the same four for fp32 (low words of a, b as floats), then
+    (mismatches, fallbacks) of the limiter-ratio division and of the Roe
+    division (b in [2^-485, 2^513])."""
     a = np.ascontiguousarray(a, dtype=np.float64)
     b = np.ascontiguousarray(b, dtype=np.float64)
     if a.shape != b.shape:
         raise ValueError("a and b must have the same shape")
-    out = (_i64 * 8)()
+    out = (_i64 * 12)()
     _check(lib().clb_selftest_arith(device, a.size, a.ctypes.data, b.ctypes.data, out))
-    return tuple(int(out[i]) for i in range(8))
+    return tuple(int(out[i]) for i in range(12))
 
 
 class PinnedBuffer:

@@ -393,6 +393,19 @@ __global__ void selftest_arith_kernel(const double* a, const double* b, int64_t 
   if (!cs && __float_as_int(sff) != __float_as_int(__fsqrt_rn(xf))) atomicAdd(&cnt[5], 1ull);
   if (cq) atomicAdd(&cnt[6], 1ull);
   if (cs) atomicAdd(&cnt[7], 1ull);
+  // limiter ratio: equal to div.rn, or both zero (the sign is free)
+  bool bl = false;
+  const double ql = clb::FastArith::div<double, clb::kChkLim>(x, y, bl);
+  const bool zeq = (__double_as_longlong(ql) << 1) == 0 && (__double_as_longlong(qr) << 1) == 0;
+  if (!bl && __double_as_longlong(ql) != __double_as_longlong(qr) && !zeq) atomicAdd(&cnt[8], 1ull);
+  if (bl) atomicAdd(&cnt[9], 1ull);
+  // Roe quotient: precondition b in [2^-485, 2^513]
+  if (y >= 0x1p-485 && y <= 0x1p513) {
+    bool br = false;
+    const double qn = clb::FastArith::div<double, clb::kChkNumNormDen>(x, y, br);
+    if (!br && __double_as_longlong(qn) != __double_as_longlong(qr)) atomicAdd(&cnt[10], 1ull);
+    if (br) atomicAdd(&cnt[11], 1ull);
+  }
 }
 
 
@@ -775,29 +788,29 @@ int clb_solve_pairs(clb_handle h, int axis, int64_t n, const void* ql, const voi
   return CLB_OK;
 }
 
-int clb_selftest_arith(int device, int64_t n, const double* a, const double* b, int64_t out[8]) {
+int clb_selftest_arith(int device, int64_t n, const double* a, const double* b, int64_t out[12]) {
   if (!a || !b || !out || n < 0) return fail(nullptr, CLB_EINVAL, "null argument");
-  for (int i = 0; i < 8; ++i) out[i] = 0;
+  for (int i = 0; i < 12; ++i) out[i] = 0;
   if (n == 0) return CLB_OK;
   if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, CLB_ECUDA, "no such device");
   double* d = nullptr;
   unsigned long long* cnt = nullptr;
   const size_t nb = (size_t)n * sizeof(double);
   cudaError_t e = cudaMalloc(&d, 2 * nb);
-  if (e == cudaSuccess) e = cudaMalloc(&cnt, 8 * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(cnt, 0, 8 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&cnt, 12 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(cnt, 0, 12 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemcpy(d, a, nb, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(d + n, b, nb, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
     selftest_arith_kernel<<<(unsigned)((n + 255) / 256), 256>>>(d, d + n, n, cnt);
     e = cudaGetLastError();
   }
-  unsigned long long h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long h[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (e == cudaSuccess) e = cudaMemcpy(h, cnt, sizeof(h), cudaMemcpyDeviceToHost);
   cudaFree(d);
   cudaFree(cnt);
   if (e != cudaSuccess) return fail(nullptr, CLB_ECUDA, cudaGetErrorString(e));
-  for (int i = 0; i < 8; ++i) out[i] = (int64_t)h[i];
+  for (int i = 0; i < 12; ++i) out[i] = (int64_t)h[i];
   return CLB_OK;
 }
 

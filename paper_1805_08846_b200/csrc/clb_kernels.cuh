@@ -40,7 +40,13 @@ enum { BC_OUTFLOW = 0, BC_REFLECTIVE = 1, BC_PERIODIC = 2, BC_HALO = 3 };
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kConsumers = 128;        // pencils per CTA
-constexpr int kThreads = kConsumers + 32;
+#ifndef CLB_INLINE_PRODUCER
+#define CLB_INLINE_PRODUCER 0
+#endif
+// CLB_INLINE_PRODUCER: consumer thread 0 issues the stage copies (no
+// producer warp), so a CTA is 4 warps
+constexpr bool kInlineProducer = CLB_INLINE_PRODUCER != 0;
+constexpr int kThreads = kConsumers + (kInlineProducer ? 0 : 32);
 constexpr int kRowStrideContig = 48;   // bytes per row per state in a contig stage
 
 // Device-resident step controller state (clb_capi.cu ctl_* kernels; the
@@ -248,7 +254,19 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 // Resident CTAs per SM the register allocation is sized for: fp64 shallow
 // water 3 (128 registers; the march would take ~168 at 2 CTAs, but the extra
 // warps win, profiles/r1_notes.md), other fp64 3, fp32 4.
+// With the inline producer a CTA is 4 warps, so the same register budget
+// fits one more CTA: fp64 shallow water 4 (strided; the TMA x-sweep stays
+// at 3, its stages fill the shared memory), other fp64 4, fp32 5.
+#ifndef CLB_SW_MINB_INL
+#define CLB_SW_MINB_INL 4
+#endif
+#ifndef CLB_SW_MINB_X_INL
+#define CLB_SW_MINB_X_INL 3
+#endif
 template <typename T, class S, bool CONTIG> constexpr int kMinBlocks() {
+  if (kInlineProducer)
+    return (sizeof(T) == 8 && S::NW >= 3) ? (CONTIG ? CLB_SW_MINB_X_INL : CLB_SW_MINB_INL)
+                                          : (sizeof(T) == 4 ? CLB_F32_MINB + 1 : CLB_F64_MINB + 1);
   return (sizeof(T) == 8 && S::NW >= 3) ? (CONTIG ? CLB_SW_MINB : CLB_SW_MINB_STRIDED)
                                         : (sizeof(T) == 4 ? CLB_F32_MINB : CLB_F64_MINB);
 }
@@ -266,8 +284,12 @@ template <typename T, class S, bool CONTIG> struct StageGeom {
   // 8192^2), per-thread stores elsewhere (acoustics y/z, which need the
   // deeper input ring: 1.45 vs 1.64 ms with staging; fp32 SW 0.83 vs 0.96)
   static constexpr int NOUT = CONTIG ? 2 : ((S::NW >= 3 && sizeof(T) == 8) ? CLB_STRIDED_OUT : 0);
+  // strided input ring: as deep as the shared memory of the resident CTAs
+  // the register budget targets allows (at most 6 stages)
+  static constexpr int BUDGET =
+      kInlineProducer ? (225 * 1024 / kMinBlocks<T, S, CONTIG>() - 1024) : 72 * 1024;
   static constexpr int NSTAGE_RAW =
-      CONTIG ? (S::M >= 4 ? 2 : CLB_CONTIG_NSTAGE) : (72 * 1024 / BYTES - NOUT);
+      CONTIG ? (S::M >= 4 ? 2 : CLB_CONTIG_NSTAGE) : (BUDGET / BYTES - NOUT);
   static constexpr int NSTAGE = NSTAGE_RAW < 2 ? 2 : (NSTAGE_RAW > 6 ? 6 : NSTAGE_RAW);
   static constexpr int SMEM = (NSTAGE + NOUT) * BYTES + 2 * NSTAGE * 8;
   static_assert(A % 3 == 2, "prologue phase");
@@ -277,30 +299,83 @@ template <typename T, class S, bool CONTIG> struct StageGeom {
 // The ring-march state of one pencil.  Slot p holds interface/cell index
 // i with i % 3 == p; P is the slot of the incoming cell.  D is the arithmetic
 // policy (clb_solvers.cuh); `bad` collects FastArith domain failures.
+#ifndef CLB_UNIFORM_SKIP
+#define CLB_UNIFORM_SKIP 1
+#endif
+
+// Bitwise equality of two cells' states.
+template <typename T, int M>
+__device__ __forceinline__ bool same_bits(const T (&a)[M], const T (&b)[M]) {
+  if constexpr (sizeof(T) == 8) {
+    unsigned long long d = 0ull;
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+      d |= (unsigned long long)(__double_as_longlong(a[k]) ^ __double_as_longlong(b[k]));
+    return d == 0ull;
+  } else {
+    uint32_t d = 0u;
+#pragma unroll
+    for (int k = 0; k < M; ++k) d |= __float_as_uint(a[k]) ^ __float_as_uint(b[k]);
+    return d == 0u;
+  }
+}
+
 template <typename T, class S, int LIM, bool LIT, class D> struct March {
   using Cell = typename S::Cell;
   using Fan = typename S::Fan;
   static constexpr int M = S::M;
+  // Uniform-state skip (exact; not in the literal blow-up kernels).  When
+  // the incoming cell i and the three before it are bitwise equal, the step
+  // is known without arithmetic:
+  //   * X[i] = X[i-1] and F[i] = F[i-1]: the same inputs give the same bits
+  //     (make / solve are pure), and |s| of F[i] is already in smax;
+  //   * every wave of a fan between equal cells is +-0 (all jumps are +0 and
+  //     each wave is a product / quotient with a jump factor), so the
+  //     correction at interface i-1 is ft = +0 + coef*(+-0) = +0 per state
+  //     (wn = +0 gives lim = 1; coef is finite);
+  //   * the update of cell i-2 adds only +-0 terms to accumulators started at
+  //     +0 and subtracts dtdx*(+0): out = q[i-2] = q[i] bitwise.
+  // "Every wave is +-0" needs the fan to be finite (a NaN root of a negative
+  // depth would make the reference's outputs NaN), so F[i-1] is tested too.
+  // A warp skips when every lane may (a warp-uniform branch).
+  static constexpr bool kSkip = !LIT && CLB_UNIFORM_SKIP != 0;
   Cell X[3];
   Fan F[3];
   T G[3][M];
   T smax;
   uint32_t fin;
   bool bad;
+  bool idle;  // lane outside the pencil block: never holds a skip back
+  int run;    // consecutive incoming cells bitwise equal to their predecessor
   T dtdx;
 
   __device__ __forceinline__ int lim(const SweepArgs<T>& a) const { return LIM >= 0 ? LIM : a.lim_id; }
 
+  __device__ __forceinline__ static bool fan_finite(Fan f) {
+    uint32_t key = 0xffffffffu;
+    S::for_regs(f, [&](T& r) { key = min(key, finite_key(r)); });
+    return key != 0u;
+  }
+  template <int P> __device__ __forceinline__ void track(const T (&q)[M]) {
+    constexpr int P1 = (P + 2) % 3;
+    if (kSkip) run = same_bits<T, M>(q, X[P1].q) ? run + 1 : 0;
+  }
   // prologue steps (no output)
   template <int P> __device__ __forceinline__ void first(const T (&q)[M]) {
     X[P] = S::template make<D>(q, bad);
+    run = 0;
   }
-  template <int P> __device__ __forceinline__ void fan(const T (&q)[M], const SweepArgs<T>& a,
-                                                       bool fold) {
+  template <int P> __device__ __forceinline__ void fan_body(const T (&q)[M],
+                                                            const SweepArgs<T>& a, bool fold) {
     constexpr int P1 = (P + 2) % 3;
     X[P] = S::template make<D>(q, bad);
     F[P] = S::template solve<D>(X[P1], X[P], a.P, bad);
     if (fold) fold_speed<S, T>(F[P], a.P, smax);
+  }
+  template <int P> __device__ __forceinline__ void fan(const T (&q)[M], const SweepArgs<T>& a,
+                                                       bool fold) {
+    track<P>(q);
+    fan_body<P>(q, a, fold);
   }
   template <int P> __device__ __forceinline__ void fan_corr(const T (&q)[M],
                                                             const SweepArgs<T>& a, bool fold) {
@@ -312,7 +387,20 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
   template <int P> __device__ __forceinline__ void step(const T (&q)[M], const SweepArgs<T>& a,
                                                         bool fold, T (&out)[M]) {
     constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
-    fan_corr<P>(q, a, fold);
+    track<P>(q);
+    if (kSkip && __all_sync(FULL, run >= 3 || idle) &&
+        __all_sync(FULL, idle || fan_finite(F[P1]))) {
+      X[P] = X[P1];
+      F[P] = F[P1];
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        G[P1][k] = T(0);
+        out[k] = q[k];
+      }
+      return;
+    }
+    fan_body<P>(q, a, fold);
+    correction<S, LIT, D, T>(F[P2], F[P1], F[P], a.P, dtdx, lim(a), G[P1], bad);
     update<S, LIT, T>(X[P2].q, F[P2], F[P1], G[P1], G[P2], a.P, dtdx, out);
   }
 };
@@ -344,49 +432,50 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   const int64_t npen = a.n1;
   const int nvalid = (int)(npen - pb < (int64_t)kConsumers ? npen - pb : (int64_t)kConsumers);
 
-  if (warp == kConsumers / 32) {
-    // ------------------------------ producer ------------------------------
+  // ------------------------------ producer ------------------------------
+  // Issue stage k of this pass into its ring slot (after the slot's previous
+  // stage was released by every consumer warp).  Run by the dedicated
+  // producer warp's lane 0, or -- CLB_INLINE_PRODUCER -- by consumer thread
+  // 0, one stage behind the march (no producer warp: its registers go to a
+  // fourth resident CTA).
+  auto produce = [&](int k) {
     constexpr int isz = (int)sizeof(T);
-    if (lane == 0) {
-      if (!CONTIG) {
-        const uint32_t colbytes = (uint32_t)(((nvalid * isz) + 15) & ~15);
-        const T* base = L.qin + pb + (int64_t)blockIdx.z * a.t2stride;
-        for (int k = 0; k < nst; ++k) {
-          const int kk = k0 + k;
-          const int s = kk % NSTAGE;
-          if (kk >= NSTAGE) mbar_wait_sleep(&empty[s], ((kk / NSTAGE) - 1) & 1);
-          const int r0 = k * NC, r1 = min(ncell, r0 + NC);
-          const int rs = max(r0, A);
-          const uint32_t bytes = (r1 > rs ? (uint32_t)(r1 - rs) : 0u) * M * colbytes;
-          mbar_arrive_expect_tx(&full[s], bytes);
-          unsigned char* st = smem + s * G::BYTES;
-          for (int r = rs; r < r1; ++r) {
-            bool neg;
-            const int js = remap(lo - 2 - A + r, a.n, a.bc_lo, a.bc_hi, neg);
-            const T* src = base + (int64_t)js * a.astride;
+    const int kk = k0 + k;
+    const int s = kk % NSTAGE;
+    if (kk >= NSTAGE) mbar_wait_sleep(&empty[s], ((kk / NSTAGE) - 1) & 1);
+    unsigned char* st = smem + s * G::BYTES;
+    if (!CONTIG) {
+      const uint32_t colbytes = (uint32_t)(((nvalid * isz) + 15) & ~15);
+      const T* base = L.qin + pb + (int64_t)blockIdx.z * a.t2stride;
+      const int r0 = k * NC, r1 = min(ncell, r0 + NC);
+      const int rs = max(r0, A);
+      const uint32_t bytes = (r1 > rs ? (uint32_t)(r1 - rs) : 0u) * M * colbytes;
+      mbar_arrive_expect_tx(&full[s], bytes);
+      for (int r = rs; r < r1; ++r) {
+        bool neg;
+        const int js = remap(lo - 2 - A + r, a.n, a.bc_lo, a.bc_hi, neg);
+        const T* src = base + (int64_t)js * a.astride;
 #pragma unroll
-            for (int q = 0; q < M; ++q)
-              bulk_g2s(st + ((q * NC + (r - r0)) * kConsumers) * isz, src + q * a.sstride,
-                       colbytes, &full[s]);
-          }
-        }
-      } else {
-        const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
-        for (int k = 0; k < nst; ++k) {
-          const int kk = k0 + k;
-          const int s = kk % NSTAGE;
-          if (kk >= NSTAGE) mbar_wait_sleep(&empty[s], ((kk / NSTAGE) - 1) & 1);
-          mbar_arrive_expect_tx(&full[s], (uint32_t)G::BYTES);
-          unsigned char* st = smem + s * G::BYTES;
-          const int cx = a.tx0 + lo - 2 - A + k * NC;
-#pragma unroll
-          for (int q = 0; q < M; ++q)
-            tma_load_4d(st + q * kConsumers * kRowStrideContig, map_ld, cx, cy, cz, q, &full[s]);
-        }
+        for (int q = 0; q < M; ++q)
+          bulk_g2s(st + ((q * NC + (r - r0)) * kConsumers) * isz, src + q * a.sstride,
+                   colbytes, &full[s]);
       }
+    } else {
+      const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
+      mbar_arrive_expect_tx(&full[s], (uint32_t)G::BYTES);
+      const int cx = a.tx0 + lo - 2 - A + k * NC;
+#pragma unroll
+      for (int q = 0; q < M; ++q)
+        tma_load_4d(st + q * kConsumers * kRowStrideContig, map_ld, cx, cy, cz, q, &full[s]);
     }
+  };
+  if (!kInlineProducer && warp == kConsumers / 32) {
+    if (lane == 0)
+      for (int k = 0; k < nst; ++k) produce(k);
     return;
   }
+  if (kInlineProducer && tid == 0)
+    for (int k = 0; k < min(nst, NSTAGE); ++k) produce(k);
   // ------------------------------ consumers ------------------------------
   const int t = tid;
   const bool active = t < nvalid;
@@ -394,6 +483,8 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   mr.smax = T(0);
   mr.fin = 0xffffffffu;
   mr.bad = false;
+  mr.idle = !active;
+  mr.run = 0;
   mr.dtdx = L.dtdx;
   const T* pin;
   T* pout;
@@ -536,6 +627,8 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   for (int k = 0; k < nst; ++k) {
     const int kk = k0 + k;
     const int s = kk % NSTAGE;
+    // inline producer: refill the slot stage k-1 used (stage k-1+NSTAGE)
+    if (kInlineProducer && t == 0 && k >= 1 && k - 1 + NSTAGE < nst) produce(k - 1 + NSTAGE);
     mbar_wait(&full[s], (kk / NSTAGE) & 1);
     unsigned char* st = smem + s * G::BYTES;
     patch(st, k);

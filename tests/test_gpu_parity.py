@@ -344,10 +344,11 @@ def _arith_inputs(rng, n):
 def test_fast_division_and_sqrt_are_bitwise_ieee(rng):
     from paper_1805_08846_b200._native import selftest_arith
     a, b = _arith_inputs(rng, 1 << 22)
-    dmis, smis, dfall, sfall, fdmis, fsmis, fdfall, fsfall = selftest_arith(a, b)
-    assert (dmis, smis, fdmis, fsmis) == (0, 0, 0, 0)
+    (dmis, smis, dfall, sfall, fdmis, fsmis, fdfall, fsfall,
+     lmis, lfall, rmis, rfall) = selftest_arith(a, b)
+    assert (dmis, smis, fdmis, fsmis, lmis, rmis) == (0, 0, 0, 0, 0, 0)
     # the edges do exercise the exact fallback
-    assert min(dfall, sfall, fdfall, fsfall) > 0
+    assert min(dfall, sfall, fdfall, fsfall, lfall, rfall) > 0
 
 
 @pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA], ids=["x-march", "x-tma"])
