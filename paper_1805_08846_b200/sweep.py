@@ -20,6 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import perf
 from ._native import DeviceGrid
 from .boundary import BC_HALO
 from .grid import GridSpec, StateGrid
@@ -163,7 +164,9 @@ def sweep_axis_tiled(q_in: StateGrid, q_out: StateGrid, axis: int, dt: float,
     smax, _ = g.sweep(axis, float(dt), 0, 1)
     _copy_ghost(q_out, q_in)
     q_out.interior()[...] = g.download(1)
-    return SweepResult(max_abs_speed=float(smax))
+    # the reference's modeled counters of this sweep (sweep.py:370-377)
+    counters, stage_flops = perf.sweep_counters(plan, spec, solver, limiter, q_in.dtype.itemsize)
+    return SweepResult(max_abs_speed=float(smax), counters=counters, stage_flops=stage_flops)
 
 
 def sweep_axis(q_in: StateGrid, q_out: StateGrid, axis: int, dt: float,
