@@ -233,6 +233,30 @@ typedef struct clb_attempt {
 
 int clb_run_batch(clb_handle h, clb_batch *b, clb_attempt *log, int64_t log_cap);
 
+/* User device Riemann solvers (the reference's plugin ABI,
+ * riemann.py:190-212 RiemannSolver + register_solver, riemann.py:259-262).
+ * A user solver is CUDA source for the scalar routine
+ *     scalar(q_l, q_r, normal, params, W_out, s_out)
+ * compiled at run time (paper_1805_08846_b200/devsolver.py, nvcc with this
+ * library's flags and headers) into a separate shared object whose entry
+ * points are registered here under an id >= CLB_SOLVER_USER_BASE.  The
+ * launch function receives the library's internal per-sweep argument block
+ * (`args`, `args_size` bytes, checked at registration) and a cudaStream_t;
+ * the pairs function is clb_solve_pairs' kernel.  Each registration fixes
+ * the state count and the dimensionality it was compiled for. */
+#define CLB_SOLVER_USER_BASE 16
+#define CLB_SOLVER_USER_MAX 64
+typedef int (*clb_user_launch_fn)(int ndim, int axis, int literal, const void *args,
+                                  void *cuda_stream);
+typedef int (*clb_user_pairs_fn)(int ndim, int axis, const void *ql, const void *qr, void *W,
+                                 void *s, int64_t n, const double *params, void *cuda_stream);
+int clb_register_device_solver(int solver_id, int ndim, int num_states, int num_waves,
+                               size_t args_size, clb_user_launch_fn launch_f32,
+                               clb_user_launch_fn launch_f64, clb_user_pairs_fn pairs_f32,
+                               clb_user_pairs_fn pairs_f64);
+/* sizeof the per-sweep argument block of this library build. */
+size_t clb_sweep_args_size(void);
+
 /* Self-test of the branch-free fp64 division / square root used by the
  * sweep kernels (clb_solvers.cuh FastArith) against div.rn.f64 /
  * sqrt.rn.f64 on n host pairs (a[i], b[i]) on device `device`.  out[0] =

@@ -36,6 +36,7 @@ EXPORTS = (
     "clb_enable_timing", "clb_timing", "clb_host_alloc", "clb_host_free", "clb_memory_info",
     "clb_selftest_arith", "clb_run_batch", "clb_frame_size", "clb_write_frame",
     "clb_sweep_segments", "clb_sweep_async_range", "clb_set_x_variant", "clb_x_variant",
+    "clb_register_device_solver", "clb_sweep_args_size",
 )
 
 #: x-sweep kernel variants (clb_set_x_variant)
@@ -113,6 +114,8 @@ def lib():
         "clb_set_stream": (_int, [_vp, _vp]),
         "clb_set_segments": (_int, [_vp, _int, _int]),
         "clb_set_x_variant": (_int, [_vp, _int]),
+        "clb_register_device_solver": (_int, [_int, _int, _int, _int, _sz, _vp, _vp, _vp, _vp]),
+        "clb_sweep_args_size": (_sz, []),
         "clb_x_variant": (_int, [_vp, ctypes.POINTER(_i32)]),
         "clb_upload": (_int, [_vp, _int, _vp, _sz]),
         "clb_download": (_int, [_vp, _int, _vp, _sz]),

@@ -87,7 +87,22 @@ int cuda_fail(clb_ctx* h, cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail((h), e_, #call); \
   } while (0)
 
+// Registered user device solvers (clb_register_device_solver).
+struct UserSolver {
+  int ndim = 0, m = 0, nw = 0;
+  clb_user_launch_fn launch[2] = {nullptr, nullptr};  // f32, f64
+  clb_user_pairs_fn pairs[2] = {nullptr, nullptr};
+};
+UserSolver g_user[CLB_SOLVER_USER_MAX];
+
+const UserSolver* user_solver(int id) {
+  if (id < CLB_SOLVER_USER_BASE || id >= CLB_SOLVER_USER_MAX) return nullptr;
+  const UserSolver* u = &g_user[id];
+  return u->launch[0] || u->launch[1] ? u : nullptr;
+}
+
 int expected_states(int solver, int ndim) {
+  if (const UserSolver* u = user_solver(solver)) return u->ndim == ndim ? u->m : -1;
   switch (solver) {
     case CLB_SOLVER_ADVECTION: return 1;
     case CLB_SOLVER_ACOUSTICS: return ndim + 1;
@@ -277,6 +292,11 @@ cudaError_t dispatch_family(clb_ctx* h, int axis, bool literal, const clb::Gener
                             cudaStream_t st) {
   const bool d64 = h->itemsize == 8;
   const int nd = h->ndim;
+  if (const UserSolver* u = user_solver(h->d.solver_id)) {
+    clb_user_launch_fn fn = u->launch[d64 ? 1 : 0];
+    if (!fn) return cudaErrorInvalidValue;
+    return (cudaError_t)fn(nd, axis, literal ? 1 : 0, &g, (void*)st);
+  }
   switch (h->d.solver_id) {
     case CLB_SOLVER_ACOUSTICS:
       return d64 ? clb::launch_acoustics_f64(nd, axis, literal, g, st)
@@ -417,6 +437,31 @@ __global__ void ctl_finish(DevCtl* c, Result* r) { ctl_finish_dev(c, r); }
 extern "C" {
 
 int clb_version(void) { return 1; }
+
+size_t clb_sweep_args_size(void) { return sizeof(clb::GenericArgs); }
+
+int clb_register_device_solver(int solver_id, int ndim, int num_states, int num_waves,
+                               size_t args_size, clb_user_launch_fn launch_f32,
+                               clb_user_launch_fn launch_f64, clb_user_pairs_fn pairs_f32,
+                               clb_user_pairs_fn pairs_f64) {
+  if (solver_id < CLB_SOLVER_USER_BASE || solver_id >= CLB_SOLVER_USER_MAX)
+    return fail(nullptr, CLB_EINVAL, "user solver ids are CLB_SOLVER_USER_BASE .. USER_MAX-1");
+  if (ndim < 1 || ndim > 3 || num_states < 1 || num_waves < 1)
+    return fail(nullptr, CLB_EINVAL, "bad user solver shape");
+  if (args_size != sizeof(clb::GenericArgs))
+    return fail(nullptr, CLB_EUNSUPPORTED,
+                "user solver compiled against a different library build (argument block size)");
+  if (!launch_f32 && !launch_f64) return fail(nullptr, CLB_EINVAL, "no launch entry point");
+  UserSolver& u = g_user[solver_id];
+  u.ndim = ndim;
+  u.m = num_states;
+  u.nw = num_waves;
+  u.launch[0] = launch_f32;
+  u.launch[1] = launch_f64;
+  u.pairs[0] = pairs_f32;
+  u.pairs[1] = pairs_f64;
+  return CLB_OK;
+}
 
 const char* clb_last_error(clb_handle h) {
   return h ? h->err.c_str() : g_create_error.c_str();
@@ -768,7 +813,9 @@ int clb_solve_pairs(clb_handle h, int axis, int64_t n, const void* ql, const voi
   if (axis < 0 || axis >= h->ndim || n < 0) return fail(h, CLB_EINVAL, "bad axis or count");
   if (n == 0) return CLB_OK;
   cudaSetDevice(h->d.device);
-  const int nw = h->d.solver_id == CLB_SOLVER_SHALLOW_WATER ? 3
+  const UserSolver* us = user_solver(h->d.solver_id);
+  const int nw = us ? us->nw
+                 : h->d.solver_id == CLB_SOLVER_SHALLOW_WATER ? 3
                  : (h->d.solver_id == CLB_SOLVER_ADVECTION ? 1 : 2);
   const size_t qb = (size_t)n * h->M * h->itemsize;
   const size_t wb = (size_t)n * nw * h->M * h->itemsize;
@@ -777,9 +824,17 @@ int clb_solve_pairs(clb_handle h, int axis, int64_t n, const void* ql, const voi
   CLB_CUDA(h, cudaMalloc(&d, 2 * qb + wb + sb));
   cudaError_t e = cudaMemcpyAsync(d, ql, qb, cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d + qb, qr, qb, cudaMemcpyHostToDevice, h->stream);
-  if (e == cudaSuccess)
-    e = clb::pairs_dispatch(h->d.solver_id, h->itemsize, h->ndim, axis, d, d + qb, d + 2 * qb,
-                            d + 2 * qb + wb, n, h->d.params, h->stream);
+  if (e == cudaSuccess) {
+    if (us) {
+      clb_user_pairs_fn fn = us->pairs[h->itemsize == 8 ? 1 : 0];
+      e = fn ? (cudaError_t)fn(h->ndim, axis, d, d + qb, d + 2 * qb, d + 2 * qb + wb, n,
+                               h->d.params, (void*)h->stream)
+             : cudaErrorInvalidValue;
+    } else {
+      e = clb::pairs_dispatch(h->d.solver_id, h->itemsize, h->ndim, axis, d, d + qb,
+                              d + 2 * qb, d + 2 * qb + wb, n, h->d.params, h->stream);
+    }
+  }
   if (e == cudaSuccess) e = cudaMemcpyAsync(W, d + 2 * qb, wb, cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(s, d + 2 * qb + wb, sb, cudaMemcpyDeviceToHost, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);

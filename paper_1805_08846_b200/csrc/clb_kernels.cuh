@@ -338,7 +338,7 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
   // "Every wave is +-0" needs the fan to be finite (a NaN root of a negative
   // depth would make the reference's outputs NaN), so F[i-1] is tested too.
   // A warp skips when every lane may (a warp-uniform branch).
-  static constexpr bool kSkip = !LIT && CLB_UNIFORM_SKIP != 0;
+  static constexpr bool kSkip = !LIT && CLB_UNIFORM_SKIP != 0 && S::kUniformSkip;
   Cell X[3];
   Fan F[3];
   T G[3][M];

@@ -124,7 +124,8 @@ def _operator(spec: GridSpec, dtype, solver: RiemannSolver, limiter: LimiterKind
         nd = spec.ndim
         g = DeviceGrid(ndim=nd, cells=spec.cells, spacing=spec.spacing,
                        num_states=spec.num_states, dtype=dtype,
-                       solver_id=solver.require_device(), limiter_id=LIMITER_IDS[limiter],
+                       solver_id=solver.require_device(spec.num_states, nd, dtype),
+                       limiter_id=LIMITER_IDS[limiter],
                        params=pv, bc=[(BC_HALO, BC_HALO)] * nd, normal_velocity=[None] * nd)
         _OPERATORS[key] = g
     return g
