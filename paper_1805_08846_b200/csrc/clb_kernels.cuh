@@ -337,7 +337,9 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
   //     +0 and subtracts dtdx*(+0): out = q[i-2] = q[i] bitwise.
   // "Every wave is +-0" needs the fan to be finite (a NaN root of a negative
   // depth would make the reference's outputs NaN), so F[i-1] is tested too.
-  // A warp skips when every lane may (a warp-uniform branch).
+  // segment_pass skips whole 3-cell groups when every lane of the warp may
+  // (a warp-uniform branch); after one skipped group all three ring slots
+  // hold the uniform state, so the next skipped groups copy nothing.
   static constexpr bool kSkip = !LIT && CLB_UNIFORM_SKIP != 0 && S::kUniformSkip;
   Cell X[3];
   Fan F[3];
@@ -346,6 +348,7 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
   uint32_t fin;
   bool bad;
   bool idle;  // lane outside the pencil block: never holds a skip back
+  bool uni;   // every ring slot holds the uniform state (a group was skipped)
   int run;    // consecutive incoming cells bitwise equal to their predecessor
   T dtdx;
 
@@ -355,6 +358,31 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
     uint32_t key = 0xffffffffu;
     S::for_regs(f, [&](T& r) { key = min(key, finite_key(r)); });
     return key != 0u;
+  }
+  // Group skip (cells i, i+1, i+2 arriving; slot 2 holds cell i-1): true
+  // when the warp may skip all three steps; then the ring is made uniform
+  // and `run` advanced.  The caller emits q0..q2 as the group's outputs.
+  __device__ __forceinline__ bool skip_group(const T (&q0)[M], const T (&q1)[M],
+                                             const T (&q2)[M]) {
+    const bool ok = idle || (run >= 2 && same_bits<T, M>(q0, X[2].q) &&
+                             same_bits<T, M>(q1, q0) && same_bits<T, M>(q2, q1));
+    if (!__all_sync(FULL, ok)) return false;
+    if (!uni) {
+      if (!__all_sync(FULL, idle || fan_finite(F[2]))) return false;
+      X[0] = X[2];
+      X[1] = X[2];
+      F[0] = F[2];
+      F[1] = F[2];
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        G[0][k] = T(0);
+        G[1][k] = T(0);
+        G[2][k] = T(0);
+      }
+      uni = true;
+    }
+    run += 3;
+    return true;
   }
   template <int P> __device__ __forceinline__ void track(const T (&q)[M]) {
     constexpr int P1 = (P + 2) % 3;
@@ -388,17 +416,6 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
                                                         bool fold, T (&out)[M]) {
     constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
     track<P>(q);
-    if (kSkip && __all_sync(FULL, run >= 3 || idle) &&
-        __all_sync(FULL, idle || fan_finite(F[P1]))) {
-      X[P] = X[P1];
-      F[P] = F[P1];
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        G[P1][k] = T(0);
-        out[k] = q[k];
-      }
-      return;
-    }
     fan_body<P>(q, a, fold);
     correction<S, LIT, D, T>(F[P2], F[P1], F[P], a.P, dtdx, lim(a), G[P1], bad);
     update<S, LIT, T>(X[P2].q, F[P2], F[P1], G[P1], G[P2], a.P, dtdx, out);
@@ -484,6 +501,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   mr.fin = 0xffffffffu;
   mr.bad = false;
   mr.idle = !active;
+  mr.uni = false;
   mr.run = 0;
   mr.dtdx = L.dtdx;
   const T* pin;
@@ -639,6 +657,21 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
       const int c0 = 3 * g;
       T q[M];
       if (r0 >= A + 4) {
+        if constexpr (decltype(mr)::kSkip) {
+          T q1[M], q2[M];
+          fetch(st, c0, q);
+          fetch(st, c0 + 1, q1);
+          fetch(st, c0 + 2, q2);
+          if (mr.skip_group(q, q1, q2)) {
+            emit(r0, r0 < ncell, q);
+            emit(r0 + 1, r0 + 1 < ncell, q1);
+            emit(r0 + 2, r0 + 2 < ncell, q2);
+            if ((CONTIG || (G::NOUT > 0 && bulk_out)) && (r0 + 2 - A - 4) % NC == NC - 1)
+              flush((r0 + 2 - A - 4) / NC);
+            continue;
+          }
+          mr.uni = false;
+        }
         T o[M];
         bool v;
         v = r0 < ncell;

@@ -442,7 +442,14 @@ def sweep_counters(plan, spec, solver, limiter, itemsize: int) -> tuple[KernelCo
 
     name = solver if isinstance(solver, str) else solver.name
     if name not in _MODEL_SCALARS:
-        raise ValueError(f"no pricing scalar for solver {name!r}")
+        # a user solver is priced by shadow-executing its own Python scalar,
+        # exactly as the reference prices every registered solver
+        scalar = getattr(solver, "scalar", None)
+        if scalar is None:
+            raise ValueError(f"no pricing scalar for solver {name!r} (give its Python "
+                             "scalar routine to price it)")
+        _MODEL_SCALARS[name] = (scalar, solver.num_waves)
+        _SAMPLE_PACKED.setdefault(name, [0.0] * 4)
     nw = _MODEL_SCALARS[name][1]
     lim_id = limiter if isinstance(limiter, int) else LIMITER_IDS[limiter]
     ev = sweep_events(plan, spec)

@@ -166,7 +166,11 @@ def sweep_axis_tiled(q_in: StateGrid, q_out: StateGrid, axis: int, dt: float,
     _copy_ghost(q_out, q_in)
     q_out.interior()[...] = g.download(1)
     # the reference's modeled counters of this sweep (sweep.py:370-377)
-    counters, stage_flops = perf.sweep_counters(plan, spec, solver, limiter, q_in.dtype.itemsize)
+    try:
+        counters, stage_flops = perf.sweep_counters(plan, spec, solver, limiter,
+                                                    q_in.dtype.itemsize)
+    except ValueError:   # a device-only user solver has no scalar to price
+        counters, stage_flops = None, {}
     return SweepResult(max_abs_speed=float(smax), counters=counters, stage_flops=stage_flops)
 
 
