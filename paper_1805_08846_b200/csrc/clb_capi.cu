@@ -158,13 +158,16 @@ bool make_tensor_map(clb_ctx* h, int buf, bool store, void* out) {
   strides[0] = (cuuint64_t)(h->ystride * isz);
   strides[1] = (cuuint64_t)(h->zstride * isz);
   strides[2] = (cuuint64_t)(h->sstride * isz);
-  cuuint32_t box[4] = {(cuuint32_t)(48 / isz), 128u, 1u, 1u};
+  // x stages: 64-byte rows (whole sectors) with the 64-byte swizzle
+  // (clb_kernels.cuh XGeom); CLB_X_LEGACY: 48-byte rows, no swizzle
+  const bool legacy = CLB_X_LEGACY != 0;
+  cuuint32_t box[4] = {(cuuint32_t)((legacy ? 48 : 64) / isz), 128u, 1u, 1u};
   cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
   CUresult r = enc((CUtensorMap*)out,
                    isz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                    h->buf[buf], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   legacy ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -241,8 +244,8 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
     }
     pen_ctas = ((nx + 127) / 128) * g.n2;
   }
-  // contig stages are 48 bytes of a row: segment starts must stay aligned
-  const int64_t align = (axis == 0 && g.contig == 2) ? 48 / h->itemsize : 1;
+  // contig stages are 64 (legacy: 48) bytes of a row: segment starts stay aligned
+  const int64_t align = (axis == 0 && g.contig == 2) ? (CLB_X_LEGACY ? 48 : 64) / h->itemsize : 1;
   static const int64_t min_seg = [] {
     const char* e = getenv("CLB_MIN_SEG");
     return e ? std::max<int64_t>(4, atoll(e)) : (int64_t)16;
@@ -511,7 +514,8 @@ int clb_create(const clb_desc* desc, clb_handle* out) {
   for (int ax = 0; ax < d.ndim; ++ax) h->cells[ax] = d.cells[ax];
   const int64_t align = 128 / d.itemsize;
   h->xoff = align;
-  // slack past the x ghosts: contig stages may read up to 13 cells beyond n+1
+  // slack past the x ghosts: contig stages may read up to 16 cells beyond n
+  // (beyond the row the TMA unit zero-fills)
   h->px = (h->xoff + h->cells[0] + 16 + align - 1) / align * align;
   h->ypad = d.ndim >= 2 ? h->cells[1] + 4 : 1;
   h->zpad = d.ndim == 3 ? h->cells[2] + 4 : 1;

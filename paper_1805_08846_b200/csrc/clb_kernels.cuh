@@ -302,6 +302,9 @@ template <typename T, class S, bool CONTIG> struct StageGeom {
 #ifndef CLB_UNIFORM_SKIP
 #define CLB_UNIFORM_SKIP 1
 #endif
+#ifndef CLB_SKIP_BACKOFF
+#define CLB_SKIP_BACKOFF 7   // most groups computed unchecked after failed checks
+#endif
 
 // Bitwise equality of two cells' states.
 template <typename T, int M>
@@ -350,6 +353,7 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
   bool idle;  // lane outside the pencil block: never holds a skip back
   bool uni;   // every ring slot holds the uniform state (a group was skipped)
   int run;    // consecutive incoming cells bitwise equal to their predecessor
+  int cool, back;  // skip-check back-off (warp-uniform)
   T dtdx;
 
   __device__ __forceinline__ int lim(const SweepArgs<T>& a) const { return LIM >= 0 ? LIM : a.lim_id; }
@@ -359,39 +363,57 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
     S::for_regs(f, [&](T& r) { key = min(key, finite_key(r)); });
     return key != 0u;
   }
-  // Group skip (cells i, i+1, i+2 arriving; slot 2 holds cell i-1): true
-  // when the warp may skip all three steps; then the ring is made uniform
-  // and `run` advanced.  The caller emits q0..q2 as the group's outputs.
-  __device__ __forceinline__ bool skip_group(const T (&q0)[M], const T (&q1)[M],
-                                             const T (&q2)[M]) {
-    const bool ok = idle || (run >= 2 && same_bits<T, M>(q0, X[2].q) &&
-                             same_bits<T, M>(q1, q0) && same_bits<T, M>(q2, q1));
-    if (!__all_sync(FULL, ok)) return false;
-    if (!uni) {
-      if (!__all_sync(FULL, idle || fan_finite(F[2]))) return false;
-      X[0] = X[2];
-      X[1] = X[2];
-      F[0] = F[2];
-      F[1] = F[2];
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        G[0][k] = T(0);
-        G[1][k] = T(0);
-        G[2][k] = T(0);
-      }
-      uni = true;
+  // Group skip (cells i, i+1, i+2 arriving; slot PP holds cell i-1): true
+  // when the warp skips all three steps; then the ring is made uniform.  The
+  // caller emits q0..q2 as the group's outputs.  `run` (consecutive incoming
+  // cells bitwise equal to their predecessor) is only maintained here; after
+  // a failed check the warp computes the next `cool` groups without checking
+  // (exponential back-off up to CLB_SKIP_BACKOFF groups), so flow that is
+  // active everywhere pays for about one check in that many groups.
+  __device__ __forceinline__ bool check_due() {
+    if (cool > 0) {
+      --cool;
+      run = 0;
+      return false;
     }
-    run += 3;
     return true;
   }
-  template <int P> __device__ __forceinline__ void track(const T (&q)[M]) {
-    constexpr int P1 = (P + 2) % 3;
-    if (kSkip) run = same_bits<T, M>(q, X[P1].q) ? run + 1 : 0;
+  template <int PP>
+  __device__ __forceinline__ bool skip_group(const T (&q0)[M], const T (&q1)[M],
+                                             const T (&q2)[M]) {
+    const bool e0 = same_bits<T, M>(q0, X[PP].q);
+    const bool e1 = same_bits<T, M>(q1, q0), e2 = same_bits<T, M>(q2, q1);
+    const bool ok = idle || (run >= 2 && e0 && e1 && e2);
+    run = e2 ? (e1 ? (e0 ? run + 3 : 2) : 1) : 0;
+    if (__all_sync(FULL, ok) && (uni || __all_sync(FULL, idle || fan_finite(F[PP])))) {
+      if (!uni) {
+        constexpr int Q1 = (PP + 1) % 3, Q2 = (PP + 2) % 3;
+        X[Q1] = X[PP];
+        X[Q2] = X[PP];
+        F[Q1] = F[PP];
+        F[Q2] = F[PP];
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          G[0][k] = T(0);
+          G[1][k] = T(0);
+          G[2][k] = T(0);
+        }
+        uni = true;
+      }
+      back = 0;
+      return true;
+    }
+    uni = false;
+    back = min(2 * back + 1, CLB_SKIP_BACKOFF);
+    cool = back;
+    return false;
   }
   // prologue steps (no output)
   template <int P> __device__ __forceinline__ void first(const T (&q)[M]) {
     X[P] = S::template make<D>(q, bad);
     run = 0;
+    cool = 0;
+    back = 0;
   }
   template <int P> __device__ __forceinline__ void fan_body(const T (&q)[M],
                                                             const SweepArgs<T>& a, bool fold) {
@@ -402,7 +424,6 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
   }
   template <int P> __device__ __forceinline__ void fan(const T (&q)[M], const SweepArgs<T>& a,
                                                        bool fold) {
-    track<P>(q);
     fan_body<P>(q, a, fold);
   }
   template <int P> __device__ __forceinline__ void fan_corr(const T (&q)[M],
@@ -415,7 +436,6 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
   template <int P> __device__ __forceinline__ void step(const T (&q)[M], const SweepArgs<T>& a,
                                                         bool fold, T (&out)[M]) {
     constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
-    track<P>(q);
     fan_body<P>(q, a, fold);
     correction<S, LIT, D, T>(F[P2], F[P1], F[P], a.P, dtdx, lim(a), G[P1], bad);
     update<S, LIT, T>(X[P2].q, F[P2], F[P1], G[P1], G[P2], a.P, dtdx, out);
@@ -503,6 +523,8 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   mr.idle = !active;
   mr.uni = false;
   mr.run = 0;
+  mr.cool = 0;
+  mr.back = 0;
   mr.dtdx = L.dtdx;
   const T* pin;
   T* pout;
@@ -657,12 +679,12 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
       const int c0 = 3 * g;
       T q[M];
       if (r0 >= A + 4) {
-        if constexpr (decltype(mr)::kSkip) {
+        if (decltype(mr)::kSkip && mr.check_due()) {
           T q1[M], q2[M];
           fetch(st, c0, q);
           fetch(st, c0 + 1, q1);
           fetch(st, c0 + 2, q2);
-          if (mr.skip_group(q, q1, q2)) {
+          if (mr.template skip_group<2>(q, q1, q2)) {
             emit(r0, r0 < ncell, q);
             emit(r0 + 1, r0 + 1 < ncell, q1);
             emit(r0 + 2, r0 + 2 < ncell, q2);
@@ -714,6 +736,240 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   bad = mr.bad && active;
 }
 
+// ---------------------------------------------------------------------------
+// The contiguous-axis (x) pass, TMA transpose with sector-aligned boxes.
+//
+// A stage is a box of NC = 64 B / itemsize cells of each of the CTA's 128 rows
+// per state (64-byte rows: whole 32-byte sectors, so the DRAM traffic is the
+// algorithmic traffic), written by the TMA engine with the 64-byte swizzle
+// (row t's 16-byte chunks XOR (t >> 1) & 3: two-way instead of four-way bank
+// conflicts when thread t reads row t).  Stage k of a segment [lo, hi) holds
+// cells lo - NC + k*NC .. lo - 1 + k*NC: stage 0 the prologue (its last four
+// cells lo-2 .. lo+1 straddle into stage 1), stage k >= 1 exactly the output
+// cells of tile k-1, so every output is written IN PLACE over its own input
+// cell (read two steps earlier by the same thread) and each stage >= 1 goes
+// back to global memory as one TMA store of the same box.  A stage's ring slot
+// is released to the producer when that store has finished reading it.
+#ifndef CLB_X_NSTAGE
+#define CLB_X_NSTAGE 3
+#endif
+#ifndef CLB_X_LEGACY
+#define CLB_X_LEGACY 0
+#endif
+template <typename T, class S> struct XGeom {
+  static constexpr int NC = 64 / (int)sizeof(T);
+  static constexpr int ROW = 64;                        // bytes per row per state
+  static constexpr int SBYTES = kConsumers * ROW;       // one state of a stage
+  static constexpr int BYTES = S::M * SBYTES;
+  static constexpr int NSTAGE = CLB_X_NSTAGE;
+  static constexpr int SMEM = NSTAGE * BYTES + 2 * NSTAGE * 8 + 1024;  // + 1024-B alignment slack
+};
+
+template <typename T, class S, int LIM, bool LIT, class D>
+__device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live<T>& L,
+                                               const TmaMaps& maps_all, unsigned char* ring,
+                                               uint64_t* full, uint64_t* empty, int k0,
+                                               T& smax, uint32_t& fin, bool& bad) {
+  using G = XGeom<T, S>;
+  constexpr int NC = G::NC, NSTAGE = G::NSTAGE, M = S::M;
+  constexpr int isz = (int)sizeof(T);
+  const unsigned char* map_ld = maps_all.ld[L.src];
+  const unsigned char* map_st = maps_all.st[L.dst];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int seg = blockIdx.y + a.seg_base;
+  const int lo = seg * a.seg_len;
+  const int hi = min(a.n, lo + a.seg_len);
+  const int len = hi - lo;
+  const int nr = len + NC + 2;                 // positions: cells lo-NC .. hi+1
+  const int nst = (nr + NC - 1) / NC;
+  const int nout = (len + NC - 1) / NC;        // output stages 1 .. nout
+  const int64_t pb = (int64_t)blockIdx.x * kConsumers;
+  const int nvalid = (int)(a.n1 - pb < (int64_t)kConsumers ? a.n1 - pb : (int64_t)kConsumers);
+  const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
+  auto slot = [&](int k) { return (k0 + k) % NSTAGE; };
+  auto stage_ptr = [&](int k) { return ring + slot(k) * G::BYTES; };
+
+  auto produce = [&](int k) {
+    const int kk = k0 + k;
+    const int s = kk % NSTAGE;
+    if (kk >= NSTAGE) mbar_wait_sleep(&empty[s], ((kk / NSTAGE) - 1) & 1);
+    mbar_arrive_expect_tx(&full[s], (uint32_t)G::BYTES);
+    const int cx = a.tx0 + lo - NC + k * NC;
+#pragma unroll
+    for (int q = 0; q < M; ++q)
+      tma_load_4d(ring + s * G::BYTES + q * G::SBYTES, map_ld, cx, cy, cz, q, &full[s]);
+  };
+  if (!kInlineProducer && warp == kConsumers / 32) {
+    if (lane == 0)
+      for (int k = 0; k < nst; ++k) produce(k);
+    return;
+  }
+  if (kInlineProducer && tid == 0)
+    for (int k = 0; k < min(nst, NSTAGE); ++k) produce(k);
+  // releases: stage k's slot goes back to the producer exactly once per pass
+  int released = 0;                             // stages 0 .. released-1 are released
+  auto release_upto = [&](int k) {              // thread 0 only
+    for (; released < k; ++released) {
+      mbar_arrive(&empty[slot(released)]);
+      if (kInlineProducer && released + NSTAGE < nst) produce(released + NSTAGE);
+    }
+  };
+
+  // ------------------------------ consumers ------------------------------
+  const int t = tid;
+  const bool active = t < nvalid;
+  const bool halo_lo = a.bc_lo == BC_HALO, halo_hi = a.bc_hi == BC_HALO;
+  // swizzled byte offset of (row t, cell c) inside one state's box
+  const int rowb = t * G::ROW;
+  const int xr = ((t >> 1) & 3) << 4;
+  auto cell_off = [&](int c) { return rowb + ((c * isz) ^ xr); };
+
+  March<T, S, LIM, LIT, D> mr;
+  mr.smax = T(0);
+  mr.fin = 0xffffffffu;
+  mr.bad = false;
+  mr.idle = !active;
+  mr.uni = false;
+  mr.run = 0;
+  mr.cool = 0;
+  mr.back = 0;
+  mr.dtdx = L.dtdx;
+  const T* pin = L.qin + (pb + (active ? t : 0)) * a.t1stride + (int64_t)blockIdx.z * a.t2stride;
+
+  // wait for stage k and fix up its physical-boundary ghosts (boundary.py
+  // semantics): the box read the memory ghosts, which are overwritten with
+  // the remapped interior value (negated for a reflective wall)
+  auto enter = [&](int k) {
+    mbar_wait(&full[slot(k)], ((k0 + k) / NSTAGE) & 1);
+    const int jlo = lo - NC + k * NC;
+    const bool any = (jlo < 0 && !halo_lo) || (jlo + NC > a.n && !halo_hi);
+    if (!any) return;
+    unsigned char* st = stage_ptr(k);
+#pragma unroll 1
+    for (int c = 0; c < NC; ++c) {
+      const int j = jlo + c;
+      const bool ghost = (j < 0 && j >= -2 && !halo_lo) || (j >= a.n && j <= a.n + 1 && !halo_hi);
+      if (!ghost) continue;
+      bool neg;
+      const int js = remap(j, a.n, a.bc_lo, a.bc_hi, neg);
+#pragma unroll
+      for (int q = 0; q < M; ++q)
+        *reinterpret_cast<T*>(st + q * G::SBYTES + cell_off(c)) =
+            neg_if(pin[js + q * a.sstride], neg && q == a.nv);
+    }
+    fence_proxy_async_smem();
+  };
+  auto fetch = [&](int r, T (&q)[M]) {
+    const unsigned char* st = stage_ptr(r / NC) + cell_off(r % NC);
+#pragma unroll
+    for (int k = 0; k < M; ++k) q[k] = *reinterpret_cast<const T*>(st + k * G::SBYTES);
+  };
+  // output cell e (position NC + e) in place; flush a completed tile
+  auto flush = [&](int k) {                     // stage k >= 1 holds tile k-1
+    fence_proxy_async_smem();
+    named_barrier_sync(1, kConsumers);
+    if (t == 0) {
+      const unsigned char* st = stage_ptr(k);
+      const int cx = a.tx0 + lo + (k - 1) * NC;
+#pragma unroll
+      for (int q = 0; q < M; ++q) tma_store_4d(map_st, st + q * G::SBYTES, cx, cy, cz, q);
+      bulk_commit();
+      // every stage before k is consumed; the store of k-1 has read its slot
+      // once at most this newest group is still reading
+      bulk_wait_read<1>();
+      release_upto(k);
+    }
+  };
+  auto emit = [&](int e, const T (&o)[M]) {
+    if (e < 0 || e >= len) return;              // (warp-uniform: e is)
+    unsigned char* st = stage_ptr(1 + e / NC) + cell_off(e % NC);
+#pragma unroll
+    for (int q = 0; q < M; ++q) *reinterpret_cast<T*>(st + q * G::SBYTES) = o[q];
+    if (active) {
+#pragma unroll
+      for (int q = 0; q < M; ++q) mr.fin = min(mr.fin, finite_key(o[q]));
+    }
+    if (e % NC == NC - 1 || e == len - 1) flush(1 + e / NC);
+  };
+  // stage transitions happen at positions r % NC == 0 (warp-uniform)
+  int entered = -1;
+  auto need = [&](int r) {
+    const int k = r / NC;
+    if (k > entered) {
+      enter(k);
+      entered = k;
+    }
+  };
+
+  // prologue: cells lo-2 .. lo+1 at positions NC-2 .. NC+1
+  constexpr int PF = (NC - 2) % 3;            // ring phase of position NC-2
+  {
+    T q[M];
+    need(0);
+    fetch(NC - 2, q);
+    mr.template first<PF>(q);
+    fetch(NC - 1, q);
+    mr.template fan<(PF + 1) % 3>(q, a, active);
+    need(NC);
+    fetch(NC, q);
+    mr.template fan<(PF + 2) % 3>(q, a, active);
+    fetch(NC + 1, q);
+    mr.template fan_corr<PF>(q, a, active);
+  }
+  // steady: position r emits cell e = r - NC - 2, phases (P0, P0+1, P0+2)
+  constexpr int P0 = (PF + 1) % 3;
+#pragma unroll 1
+  for (int r = NC + 2; r < nr; r += 3) {
+    const bool v1 = r + 1 < nr, v2 = r + 2 < nr;
+    T q[M];
+    if constexpr (decltype(mr)::kSkip) {
+      if (v2 && mr.check_due()) {
+        T q1[M], q2[M];
+        need(r);
+        fetch(r, q);
+        need(r + 1);
+        fetch(r + 1, q1);
+        need(r + 2);
+        fetch(r + 2, q2);
+        if (mr.template skip_group<(P0 + 2) % 3>(q, q1, q2)) {
+          emit(r - NC - 2, q);
+          emit(r - NC - 1, q1);
+          emit(r - NC, q2);
+          continue;
+        }
+        mr.uni = false;
+      }
+    }
+    T o[M];
+    need(r);
+    fetch(r, q);
+    mr.template step<P0>(q, a, active, o);
+    emit(r - NC - 2, o);
+    if (!v1) break;
+    need(r + 1);
+    fetch(r + 1, q);
+    mr.template step<(P0 + 1) % 3>(q, a, active, o);
+    emit(r - NC - 1, o);
+    if (!v2) break;
+    need(r + 2);
+    fetch(r + 2, q);
+    mr.template step<(P0 + 2) % 3>(q, a, active, o);
+    emit(r - NC, o);
+  }
+  // every slot of the pass goes back once; the stores have completed before
+  // the next pass (or the kernel) ends
+  named_barrier_sync(1, kConsumers);
+  if (t == 0) {
+    bulk_wait<0>();
+    release_upto(nst);
+  }
+  smax = mr.smax;
+  fin = mr.fin;
+  bad = mr.bad && active;
+  (void)nout;
+}
+
 // Number of stages one segment pass streams (same formula as segment_pass).
 template <typename T, class S, bool CONTIG>
 __device__ __forceinline__ int segment_stages(const SweepArgs<T>& a) {
@@ -739,16 +995,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S, CONTIG>())
     sweep_kernel(const SweepArgs<T> a, const __grid_constant__ TmaMaps maps) {
   Live<T> L;
   if (!resolve_live(a, L)) return;
+  constexpr bool XNEW = CONTIG && !CLB_X_LEGACY;
   using G = StageGeom<T, S, CONTIG>;
-  constexpr int NSTAGE = G::NSTAGE;
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (NSTAGE + G::NOUT) * G::BYTES);
+  constexpr int NSTAGE = XNEW ? XGeom<T, S>::NSTAGE : G::NSTAGE;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // the swizzled x stages need 1024-byte aligned buffers
+  unsigned char* smem = XNEW ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u)
+                             : smem_raw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(
+      smem + (XNEW ? NSTAGE * XGeom<T, S>::BYTES : (NSTAGE + G::NOUT) * G::BYTES));
   uint64_t* empty = full + NSTAGE;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers / 32);
+      // x stages are released by one thread after their store read them
+      mbar_init(&empty[s], XNEW ? 1 : kConsumers / 32);
     }
     fence_mbar_init();
   }
@@ -757,21 +1019,36 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T, S, CONTIG>())
   T smax = T(0);
   uint32_t fin = 0xffffffffu;
   bool bad = false;
+  auto pass = [&](auto arith, int k0) {
+    using D = decltype(arith);
+    if constexpr (XNEW)
+      segment_pass_x<T, S, LIM, LIT, D>(a, L, maps, smem, full, empty, k0, smax, fin, bad);
+    else
+      segment_pass<T, S, LIM, LIT, CONTIG, D>(a, L, maps, smem, full, empty, k0, smax, fin, bad);
+  };
+  auto stages = [&]() {
+    if constexpr (XNEW) {
+      const int lo = (blockIdx.y + a.seg_base) * a.seg_len;
+      const int len = min(a.n, lo + a.seg_len) - lo;
+      constexpr int NC = XGeom<T, S>::NC;
+      return (len + NC + 2 + NC - 1) / NC;
+    } else {
+      return segment_stages<T, S, CONTIG>(a);
+    }
+  };
   // fp32 shallow water: the exact fp32 division (zero numerators short-cut)
   // beats the fp64-pipe fast path (8 divisions per cell; y 0.99 vs 1.33 ms at
   // 8192^2); acoustics' two limiter divisions meet tiny far-field waves that
   // send div.rn.f32 to its slow path, so it keeps the fast path (1.09 vs 1.35)
   if (LIT || (sizeof(T) == 4 && (S::NW >= 3 || CLB_EXACT32))) {
-    segment_pass<T, S, LIM, LIT, CONTIG, ExactArith>(a, L, maps, smem, full, empty, 0, smax, fin, bad);
+    pass(ExactArith{}, 0);
   } else {
-    segment_pass<T, S, LIM, LIT, CONTIG, FastArith>(a, L, maps, smem, full, empty, 0, smax, fin, bad);
+    pass(FastArith{}, 0);
     // CLB_NO_REDO: timing experiments only (results may differ from div.rn)
     if (__syncthreads_or(bad) && !CLB_NO_REDO) {
       smax = T(0);
       fin = 0xffffffffu;
-      const int k0 = segment_stages<T, S, CONTIG>(a);
-      segment_pass<T, S, LIM, LIT, CONTIG, ExactArith>(a, L, maps, smem, full, empty, k0, smax,
-                                                       fin, bad);
+      pass(ExactArith{}, stages());
     }
   }
   finish_block<T>(smax, fin, a);
@@ -1068,7 +1345,8 @@ inline cudaError_t launch_contig_shfl(const GenericArgs& g, cudaStream_t st) {
 template <typename T, class S, int LIM, bool LIT, bool CONTIG>
 inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
   if (CONTIG && g.contig == 1) return launch_contig_shfl<T, S, LIM, LIT>(g, st);
-  using Geo = StageGeom<T, S, CONTIG>;
+  constexpr int kSmem = (CONTIG && !CLB_X_LEGACY) ? XGeom<T, S>::SMEM
+                                                   : StageGeom<T, S, CONTIG>::SMEM;
   // the dynamic shared-memory opt-in is per device: one bit per device
   // ordinal, set once (atomically: service threads may launch concurrently)
   static std::atomic<unsigned long long> configured{0ull};
@@ -1077,17 +1355,17 @@ inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(configured.load(std::memory_order_acquire) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Geo::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
     configured.fetch_or(bit, std::memory_order_release);
   }
   if (g.occ_out) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(g.occ_out, fn, kThreads,
-                                                                      Geo::SMEM);
+                                                                      kSmem);
   SweepArgs<T> a = to_args<T>(g);
   static const TmaMaps none{};
   dim3 grid((unsigned)((g.n1 + kConsumers - 1) / kConsumers), (unsigned)(g.seg_end - g.seg_begin),
             (unsigned)g.n2);
-  fn<<<grid, kThreads, Geo::SMEM, st>>>(a, CONTIG ? *g.maps : none);
+  fn<<<grid, kThreads, kSmem, st>>>(a, CONTIG ? *g.maps : none);
   return cudaGetLastError();
 }
 
