@@ -107,8 +107,8 @@ def config_of(args, world, scaling):
         "cells": list(gcells),
         "scaling": scaling,
         "parallelism": (f"slab x{world} along the slowest axis, NCCL halo exchange "
-                        "(overlapped with the slow sweep) + max-allreduce" if world > 1
-                        else "single GPU"),
+                        "(overlapped with the slow sweep) + max-allreduce on the device"
+                        if world > 1 else "single GPU"),
         "l2": "flushed between steps (1 GiB write, untimed); the grid is larger than L2"
               if int(np.prod(gcells)) * 8 > 126e6 else
               "flushed between steps (1 GiB write, untimed); the working set fits L2",
@@ -436,6 +436,8 @@ def run_gpu(args, rank, world, scaling):
            "d2h_bytes_per_step": int(state_bytes / args.steps + rec_bytes * e2e_att / args.steps),
            "api": "Simulation.run_until(max_steps=K)"
                   + (" (device-resident controller, one batch)" if world == 1 else
+                     " (device-resident controller; halo exchange and max-allreduce over "
+                     "NCCL inside the attempt graph)" if args.transport == "device" else
                      " (per-attempt host loop with NCCL halo exchange + max-allreduce)")
                   + ": pinned H2D upload of the state, K steps, D2H of the state and the "
                     "attempt records; wall clock, max over ranks",
@@ -495,8 +497,10 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "host"],
-                    help="halo transport for N>1 (host: gloo, for ranks sharing one GPU)")
+    ap.add_argument("--transport", default="device", choices=["device", "nccl", "host"],
+                    help="halo transport for N>1: device (NCCL inside the library, exchange "
+                         "and max-allreduce in the attempt graph), nccl (torch NCCL per "
+                         "attempt), host (gloo, for ranks sharing one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     scaling = args.scaling or DEFAULT_SCALING.get(args.workload, "weak")

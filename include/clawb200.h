@@ -257,6 +257,28 @@ int clb_register_device_solver(int solver_id, int ndim, int num_states, int num_
 /* sizeof the per-sweep argument block of this library build. */
 size_t clb_sweep_args_size(void);
 
+/* Slab decomposition on the device (slab.py).  Each rank's
+ * handle owns its slab of the global grid (slowest axis split); the slow-axis
+ * sides with a neighbour are CLB_BC_HALO.  clb_attach_comm creates an NCCL
+ * communicator (NCCL is loaded at run time; `id` is the 128-byte
+ * ncclUniqueId from clb_nccl_unique_id on one rank, broadcast by the caller)
+ * and from then on every attempt -- clb_attempt_step and the attempt graph
+ * of clb_run_batch -- exchanges the 2 boundary rows/planes of every state
+ * with the neighbours before the slow sweep (pack into fixed staging
+ * buffers, ncclSend/ncclRecv on a side stream while the slow sweep's
+ * interior segments run, unpack into the ghost layers) and max-allreduces
+ * the per-sweep (max |s|, non-finite) results before they are read, so the
+ * fp64 controller takes the identical decision on every rank.  lo_nbr /
+ * hi_nbr: neighbour ranks (-1 = physical boundary); a rank may be its own
+ * neighbour (a periodic axis on one rank).  Collective over the ranks. */
+int clb_nccl_unique_id(void *id_out /* 128 bytes */);
+int clb_attach_comm(clb_handle h, const void *id, int nranks, int rank, int lo_nbr, int hi_nbr);
+/* The exchange alone into buffer `buf`'s ghost layers (blow-up slow path). */
+int clb_halo_exchange(clb_handle h, int buf);
+/* Max-allreduce of the accumulated per-sweep result slots (no-op without a
+ * communicator); clb_fetch then reads the global values. */
+int clb_results_allreduce(clb_handle h);
+
 /* Self-test of the branch-free fp64 division / square root used by the
  * sweep kernels (clb_solvers.cuh FastArith) against div.rn.f64 /
  * sqrt.rn.f64 on n host pairs (a[i], b[i]) on device `device`.  out[0] =

@@ -36,7 +36,8 @@ EXPORTS = (
     "clb_enable_timing", "clb_timing", "clb_host_alloc", "clb_host_free", "clb_memory_info",
     "clb_selftest_arith", "clb_run_batch", "clb_frame_size", "clb_write_frame",
     "clb_sweep_segments", "clb_sweep_async_range", "clb_set_x_variant", "clb_x_variant",
-    "clb_register_device_solver", "clb_sweep_args_size",
+    "clb_register_device_solver", "clb_sweep_args_size", "clb_nccl_unique_id",
+    "clb_attach_comm", "clb_halo_exchange", "clb_results_allreduce",
 )
 
 #: x-sweep kernel variants (clb_set_x_variant)
@@ -116,6 +117,10 @@ def lib():
         "clb_set_x_variant": (_int, [_vp, _int]),
         "clb_register_device_solver": (_int, [_int, _int, _int, _int, _sz, _vp, _vp, _vp, _vp]),
         "clb_sweep_args_size": (_sz, []),
+        "clb_nccl_unique_id": (_int, [_vp]),
+        "clb_attach_comm": (_int, [_vp, _vp, _int, _int, _int, _int]),
+        "clb_halo_exchange": (_int, [_vp, _int]),
+        "clb_results_allreduce": (_int, [_vp]),
         "clb_x_variant": (_int, [_vp, ctypes.POINTER(_i32)]),
         "clb_upload": (_int, [_vp, _int, _vp, _sz]),
         "clb_download": (_int, [_vp, _int, _vp, _sz]),
@@ -263,6 +268,19 @@ class DeviceGrid:
         _check(lib().clb_x_variant(self.handle, ctypes.byref(v)), self.handle)
         return int(v.value)
 
+    def attach_comm(self, uid: bytes, nranks: int, rank: int, lo_nbr, hi_nbr):
+        """Device-resident slab exchange over NCCL (clb_attach_comm)."""
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        _check(lib().clb_attach_comm(self.handle, buf, int(nranks), int(rank),
+                                     -1 if lo_nbr is None else int(lo_nbr),
+                                     -1 if hi_nbr is None else int(hi_nbr)), self.handle)
+
+    def halo_exchange(self, buf: int):
+        _check(lib().clb_halo_exchange(self.handle, int(buf)), self.handle)
+
+    def results_allreduce(self):
+        _check(lib().clb_results_allreduce(self.handle), self.handle)
+
     def set_stream(self, stream_ptr: int | None):
         _check(lib().clb_set_stream(self.handle, stream_ptr or None), self.handle)
 
@@ -377,6 +395,13 @@ class DeviceGrid:
         p = _i64()
         _check(lib().clb_memory_info(self.handle, ctypes.byref(b), ctypes.byref(p)), self.handle)
         return b.value, p.value
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (clb_nccl_unique_id)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().clb_nccl_unique_id(buf))
+    return buf.raw
 
 
 def selftest_arith(a, b, device: int = 0):

@@ -15,6 +15,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -22,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/clawb200.h"
@@ -36,6 +39,7 @@ using clb::Result;
 struct TimedLaunch {
   int axis;
   cudaEvent_t a, b;
+  int counts;   // 0 for the later segment-range launches of one sweep
 };
 
 }  // namespace
@@ -65,6 +69,17 @@ struct clb_ctx {
   cudaGraph_t batch_graph = nullptr;
   bool have_maps = false;
   bool timing = false;
+  // slab decomposition (clb_attach_comm): slow-axis halo exchange over NCCL
+  // between fixed staging buffers, and the max-allreduce of the per-sweep
+  // results, both on the device (inside the attempt graph of clb_run_batch)
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  int nbr[2] = {-1, -1};          // rank below / above on the slow axis (-1: none)
+  size_t halo_block = 0;          // bytes of 2 rows/planes of one state
+  int64_t halo_send_off[2] = {0, 0}, halo_recv_off[2] = {0, 0};  // byte offsets in a buffer
+  char* halo_stage = nullptr;     // [send lo, send hi, recv lo, recv hi][M][halo_block]
+  cudaStream_t side = nullptr;    // exchange stream (overlaps the slow sweep's interior)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<TimedLaunch> launches;
   std::vector<cudaEvent_t> event_pool;
   std::string err;
@@ -316,6 +331,151 @@ cudaError_t dispatch_family(clb_ctx* h, int axis, bool literal, const clb::Gener
   }
 }
 
+// NCCL, loaded at run time (the library does not link it): torch's copy
+// when torch is already in the process (same soname), else the system one.
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* lib = nullptr;
+    const char* env = getenv("CLB_NCCL_LIB");
+    for (const char* name : {env, "libnccl.so.2", "libnccl.so"}) {
+      if (!name) continue;
+      lib = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (lib) break;
+    }
+    if (!lib) { a.err = "libnccl.so.2 not found"; return a; }
+    bool all = true;
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(lib, name));
+      all = all && fn != nullptr;
+    };
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.AllReduce, "ncclAllReduce");
+    sym(a.Send, "ncclSend");
+    sym(a.Recv, "ncclRecv");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    a.ok = all;
+    if (!all) a.err = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+int nccl_fail(clb_ctx* h, ncclResult_t r, const char* where) {
+  const NcclApi& n = nccl();
+  return fail(h, CLB_ECUDA, std::string(where) + ": " +
+                                (n.GetErrorString ? n.GetErrorString(r) : "nccl error"));
+}
+
+#define CLB_NCCL(h, call)                                        \
+  do {                                                           \
+    ncclResult_t r_ = (call);                                    \
+    if (r_ != ncclSuccess) return nccl_fail((h), r_, #call);     \
+  } while (0)
+
+// Halo pack / unpack between a buffer's 2 boundary rows/planes (per state a
+// contiguous block) and the staging area.  Indirect (ctl != null): the
+// buffer is the controller's input of the slow sweep, and a finished
+// controller makes them no-ops (graph replays past the end of a run).
+struct HaloArgs {
+  const clb::DevCtl* ctl;
+  int slow;                 // slow axis (the sweep whose input is exchanged)
+  int buf;                  // direct launches
+  char* bufs[3];
+  int64_t off[2];           // byte offset of the side's block in a buffer
+  int64_t sstride;          // bytes between states
+  int64_t block;            // bytes per state and side (multiple of 16)
+  int m;
+  int side_mask;            // bit s: side s has a neighbour
+  char* stage;              // [2 sides][m][block]
+};
+
+__global__ void halo_copy_kernel(HaloArgs a, int unpack) {
+  if (a.ctl && a.ctl->done) return;
+  const int b = a.ctl ? a.ctl->src[a.slow] : a.buf;
+  char* base = a.bufs[b];
+  const int64_t nvec = a.block / 16;
+  for (int side = 0; side < 2; ++side) {
+    if (!(a.side_mask >> side & 1)) continue;
+    for (int k = 0; k < a.m; ++k) {
+      uint4* g = reinterpret_cast<uint4*>(base + a.off[side] + k * a.sstride);
+      uint4* st = reinterpret_cast<uint4*>(a.stage + ((int64_t)side * a.m + k) * a.block);
+      for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+           i += (int64_t)gridDim.x * blockDim.x) {
+        if (unpack) g[i] = st[i]; else st[i] = g[i];
+      }
+    }
+  }
+}
+
+HaloArgs halo_args(clb_ctx* h, bool recv, int buf, bool indirect) {
+  HaloArgs a;
+  a.ctl = indirect ? h->d_ctl : nullptr;
+  a.slow = h->ndim - 1;
+  a.buf = buf;
+  for (int i = 0; i < 3; ++i) a.bufs[i] = (char*)h->buf[i];
+  for (int s = 0; s < 2; ++s) a.off[s] = recv ? h->halo_recv_off[s] : h->halo_send_off[s];
+  a.sstride = h->sstride * h->itemsize;
+  a.block = (int64_t)h->halo_block;
+  a.m = h->M;
+  a.side_mask = (h->nbr[0] >= 0 ? 1 : 0) | (h->nbr[1] >= 0 ? 2 : 0);
+  a.stage = h->halo_stage + (recv ? 2 : 0) * (size_t)h->M * h->halo_block;
+  return a;
+}
+
+// pack -> send/recv -> unpack on stream `st`.  NCCL pairs the messages of
+// two ranks in posting order, so the order is canonical: send the hi rows,
+// then the lo rows; receive into the lo ghosts, then the hi ghosts (which
+// also pairs a 2-rank periodic ring and a rank exchanging with itself).
+int halo_exchange_on(clb_ctx* h, cudaStream_t st, int buf, bool indirect) {
+  const NcclApi& n = nccl();
+  const int blocks = (int)std::min<int64_t>((h->halo_block / 16 + 255) / 256 * 2, 4 * h->num_sms);
+  halo_copy_kernel<<<std::max(blocks, 1), 256, 0, st>>>(halo_args(h, false, buf, indirect), 0);
+  CLB_CUDA(h, cudaGetLastError());
+  const size_t bytes = (size_t)h->M * h->halo_block;
+  char* send = h->halo_stage;
+  char* recv = h->halo_stage + 2 * bytes;
+  CLB_NCCL(h, n.GroupStart());
+  if (h->nbr[1] >= 0) CLB_NCCL(h, n.Send(send + bytes, bytes, ncclUint8, h->nbr[1], h->comm, st));
+  if (h->nbr[0] >= 0) CLB_NCCL(h, n.Send(send, bytes, ncclUint8, h->nbr[0], h->comm, st));
+  if (h->nbr[0] >= 0) CLB_NCCL(h, n.Recv(recv, bytes, ncclUint8, h->nbr[0], h->comm, st));
+  if (h->nbr[1] >= 0) CLB_NCCL(h, n.Recv(recv + bytes, bytes, ncclUint8, h->nbr[1], h->comm, st));
+  CLB_NCCL(h, n.GroupEnd());
+  halo_copy_kernel<<<std::max(blocks, 1), 256, 0, st>>>(halo_args(h, true, buf, indirect), 1);
+  CLB_CUDA(h, cudaGetLastError());
+  return CLB_OK;
+}
+
+// max over ranks of the per-sweep results: non-negative doubles order as
+// their bit patterns (uint64 max), flags as int32 max; exact, order-free.
+int results_allreduce(clb_ctx* h, cudaStream_t st) {
+  const NcclApi& n = nccl();
+  CLB_NCCL(h, n.AllReduce(h->d_res->smax, h->d_res->smax, (size_t)h->ndim, ncclUint64, ncclMax,
+                          h->comm, st));
+  CLB_NCCL(h, n.AllReduce(h->d_res->nonfinite, h->d_res->nonfinite, (size_t)h->ndim, ncclInt32,
+                          ncclMax, h->comm, st));
+  return CLB_OK;
+}
+
 // indirect: buffers and dt are read by the kernel from h->d_ctl (batch graphs)
 int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bool literal,
                  bool indirect = false, int seg_begin = 0, int seg_end = -1, bool fuse = false) {
@@ -342,7 +502,7 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
   for (int i = 0; i < 4; ++i) g.params[i] = h->d.params[i];
   g.smax_bits = &h->d_res->smax[slot];
   g.nonfinite = &h->d_res->nonfinite[slot];
-  TimedLaunch tl{axis, nullptr, nullptr};
+  TimedLaunch tl{axis, nullptr, nullptr, (seg_end < 0 || seg_begin == 0) ? 1 : 0};
   if (h->timing && !indirect) {
     tl.a = take_event(h);
     tl.b = take_event(h);
@@ -355,6 +515,49 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
     h->launches.push_back(tl);
   }
   return CLB_OK;
+}
+
+// The slow-axis sweep overlapped with its halo exchange (slab.py
+// slow_sweep, on the device): the segments whose rows stay clear of the
+// ghost layers run on the main stream while pack / send / recv / unpack run
+// on the side stream; the two edge groups follow the join.  Segments are
+// independent, so this is bitwise one exchange followed by one sweep.
+int slow_sweep_exchange(clb_ctx* h, double dt, int src, int dst, int slot, bool literal,
+                        bool indirect) {
+  const int axis = h->ndim - 1;
+  const clb::GenericArgs g = sweep_geometry(h, axis, 0, 1);
+  const int64_t n = h->cells[axis], L = g.seg_len;
+  int b = -1, e = -1;
+  for (int k = 0; k < g.nseg; ++k) {
+    if ((int64_t)k * L >= 2 && std::min<int64_t>(n, (int64_t)(k + 1) * L) + 2 <= n) {
+      if (b < 0) b = k;
+      e = k + 1;
+    }
+  }
+  CLB_CUDA(h, cudaEventRecord(h->ev_fork, h->stream));
+  CLB_CUDA(h, cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+  int r = halo_exchange_on(h, h->side, src, indirect);
+  if (r) return r;
+  CLB_CUDA(h, cudaEventRecord(h->ev_join, h->side));
+  if (b >= 0) {
+    r = launch_sweep(h, axis, dt, src, dst, slot, literal, indirect, b, e);
+    if (r) return r;
+  }
+  CLB_CUDA(h, cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+  if (b < 0) return launch_sweep(h, axis, dt, src, dst, slot, literal, indirect);
+  if (b > 0) {
+    r = launch_sweep(h, axis, dt, src, dst, slot, literal, indirect, 0, b);
+    if (r) return r;
+  }
+  if (e < g.nseg) return launch_sweep(h, axis, dt, src, dst, slot, literal, indirect, e, g.nseg);
+  return CLB_OK;
+}
+
+// one sweep of an attempt: the slow axis of a slab exchanges its halo first
+int attempt_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bool literal,
+                  bool indirect) {
+  if (h->comm && axis == h->ndim - 1) return slow_sweep_exchange(h, dt, src, dst, slot, literal, indirect);
+  return launch_sweep(h, axis, dt, src, dst, slot, literal, indirect);
 }
 
 int fetch(clb_ctx* h, int nslots, double* speeds, int32_t* nonfinite) {
@@ -572,6 +775,11 @@ int clb_destroy(clb_handle h) {
   if (h->d_ctl) cudaFree(h->d_ctl);
   if (h->h_ctl) cudaFreeHost(h->h_ctl);
   if (h->d_log) cudaFree(h->d_log);
+  if (h->comm) nccl().CommDestroy(h->comm);
+  if (h->halo_stage) cudaFree(h->halo_stage);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;
   return CLB_OK;
@@ -745,9 +953,13 @@ int clb_attempt_step(clb_handle h, double dt, int src, int s0, int s1, double* s
   int cur = src;
   for (int j = 0; j < h->ndim; ++j) {
     const int dst = (j % 2 == 0) ? s0 : s1;
-    int r = launch_sweep(h, j, dt, cur, dst, j, false);
+    int r = attempt_sweep(h, j, dt, cur, dst, j, false, false);
     if (r) return r;
     cur = dst;
+  }
+  if (h->comm) {
+    const int r = results_allreduce(h, h->stream);
+    if (r) return r;
   }
   return fetch(h, h->ndim, speeds, nonfinite);
 }
@@ -887,7 +1099,7 @@ int clb_timing(clb_handle h, double ms[3], int64_t count[3]) {
     float v = 0.f;
     cudaEventElapsedTime(&v, tl.a, tl.b);
     ms[tl.axis] += v;
-    count[tl.axis] += 1;
+    count[tl.axis] += tl.counts;
     h->event_pool.push_back(tl.a);
     h->event_pool.push_back(tl.b);
   }
@@ -1001,9 +1213,17 @@ int build_batch_graph(clb_ctx* h) {
     return e && e[0] == '1';
   }();
   int r = 0;
-  for (int j = 0; j < h->ndim && !r; ++j)
-    r = launch_sweep(h, j, 1.0, 0, 1, j, false, true, 0, -1, fused && j == h->ndim - 1);
-  if (!r && !fused) clb::ctl_finish<<<1, 1, 0, h->stream>>>(h->d_ctl, h->d_res);
+  if (h->comm) {
+    // slab: halo exchange inside the slow sweep, max-allreduce of the
+    // results before the controller (no host round trip per attempt)
+    for (int j = 0; j < h->ndim && !r; ++j) r = attempt_sweep(h, j, 1.0, 0, 1, j, false, true);
+    if (!r) r = results_allreduce(h, h->stream);
+    if (!r) clb::ctl_finish<<<1, 1, 0, h->stream>>>(h->d_ctl, h->d_res);
+  } else {
+    for (int j = 0; j < h->ndim && !r; ++j)
+      r = launch_sweep(h, j, 1.0, 0, 1, j, false, true, 0, -1, fused && j == h->ndim - 1);
+    if (!r && !fused) clb::ctl_finish<<<1, 1, 0, h->stream>>>(h->d_ctl, h->d_res);
+  }
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(h->stream, &g);
   if (r) { if (g) cudaGraphDestroy(g); return r; }
@@ -1099,4 +1319,74 @@ extern "C" int clb_run_batch(clb_handle h, clb_batch* b, clb_attempt* log, int64
   b->fail_sweep = c.fail_sweep;
   b->fail_dt = c.dt;
   return CLB_OK;
+}
+
+extern "C" int clb_nccl_unique_id(void* id_out) {
+  if (!id_out) return fail(nullptr, CLB_EINVAL, "null argument");
+  const NcclApi& n = nccl();
+  if (!n.ok) return fail(nullptr, CLB_EUNSUPPORTED, "NCCL unavailable: " + n.err);
+  ncclUniqueId id;
+  const ncclResult_t r = n.GetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(nullptr, r, "ncclGetUniqueId");
+  std::memcpy(id_out, &id, sizeof(id));
+  return CLB_OK;
+}
+
+extern "C" int clb_attach_comm(clb_handle h, const void* id, int nranks, int rank, int lo_nbr,
+                               int hi_nbr) {
+  if (!h || !id) return fail(h, CLB_EINVAL, "null argument");
+  if (h->ndim < 2) return fail(h, CLB_EUNSUPPORTED, "slab exchange needs ndim >= 2");
+  if (h->comm) return fail(h, CLB_EINVAL, "a communicator is already attached");
+  if (nranks < 1 || rank < 0 || rank >= nranks || lo_nbr < -1 || lo_nbr >= nranks ||
+      hi_nbr < -1 || hi_nbr >= nranks)
+    return fail(h, CLB_EINVAL, "bad rank / neighbour");
+  const int slow = h->ndim - 1;
+  if ((lo_nbr >= 0 && h->d.bc[slow][0] != CLB_BC_HALO) ||
+      (hi_nbr >= 0 && h->d.bc[slow][1] != CLB_BC_HALO))
+    return fail(h, CLB_EINVAL, "a side with a neighbour must be a CLB_BC_HALO side");
+  const NcclApi& n = nccl();
+  if (!n.ok) return fail(h, CLB_EUNSUPPORTED, "NCCL unavailable: " + n.err);
+  CLB_CUDA(h, cudaSetDevice(h->d.device));
+  void *send_lo, *recv_lo, *send_hi, *recv_hi;
+  size_t bb = 0, ss = 0;
+  int r = clb_halo_layout(h, 0, 0, &send_lo, &recv_lo, &bb, &ss);
+  if (!r) r = clb_halo_layout(h, 0, 1, &send_hi, &recv_hi, &bb, &ss);
+  if (r) return r;
+  const char* b0 = (const char*)h->buf[0];
+  h->halo_send_off[0] = (const char*)send_lo - b0;
+  h->halo_send_off[1] = (const char*)send_hi - b0;
+  h->halo_recv_off[0] = (const char*)recv_lo - b0;
+  h->halo_recv_off[1] = (const char*)recv_hi - b0;
+  h->halo_block = bb;
+  CLB_CUDA(h, cudaMalloc(&h->halo_stage, 4 * (size_t)h->M * bb));
+  CLB_CUDA(h, cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  CLB_CUDA(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  CLB_CUDA(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm = nullptr;
+  const ncclResult_t nr = n.CommInitRank(&comm, nranks, uid, rank);
+  if (nr != ncclSuccess) return nccl_fail(h, nr, "ncclCommInitRank");
+  h->comm = comm;
+  h->nranks = nranks;
+  h->rank = rank;
+  h->nbr[0] = lo_nbr;
+  h->nbr[1] = hi_nbr;
+  drop_batch_graph(h);
+  return CLB_OK;
+}
+
+extern "C" int clb_halo_exchange(clb_handle h, int buf) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  if (!h->comm) return fail(h, CLB_EINVAL, "no communicator attached");
+  if (buf < 0 || buf > 2) return fail(h, CLB_EINVAL, "buffer index out of range");
+  cudaSetDevice(h->d.device);
+  return halo_exchange_on(h, h->stream, buf, false);
+}
+
+extern "C" int clb_results_allreduce(clb_handle h) {
+  if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
+  if (!h->comm) return CLB_OK;
+  cudaSetDevice(h->d.device);
+  return results_allreduce(h, h->stream);
 }

@@ -66,18 +66,29 @@ class SlabLayout:
     offset: int               # first global index owned along `axis`
     count: int                # owned cells along `axis`
     periodic: bool
+    # a periodic slow axis wraps through the exchange even on one rank (the
+    # rank is its own neighbour): the single-GPU check of the device path
+    self_halo: bool = False
+
+    @property
+    def _wraps(self):
+        return self.periodic and (self.world > 1 or self.self_halo)
 
     @property
     def lo_nbr(self):
         if self.rank > 0:
             return self.rank - 1
-        return self.world - 1 if (self.periodic and self.world > 1) else None
+        return self.world - 1 if self._wraps else None
 
     @property
     def hi_nbr(self):
         if self.rank < self.world - 1:
             return self.rank + 1
-        return 0 if (self.periodic and self.world > 1) else None
+        return 0 if self._wraps else None
+
+    @property
+    def exchanges(self):
+        return self.lo_nbr is not None or self.hi_nbr is not None
 
 
 class Slab:
@@ -88,7 +99,7 @@ class Slab:
     """
 
     def __init__(self, global_spec: GridSpec, boundary, rank: int = 0, world: int = 1,
-                 dist=None, transport: str = "nccl", group=None):
+                 dist=None, transport: str = "nccl", group=None, self_halo: bool = False):
         if global_spec.ndim < 2 and world > 1:
             raise ValueError("slab decomposition needs ndim >= 2")
         self.global_spec = global_spec
@@ -96,8 +107,10 @@ class Slab:
         axis = global_spec.ndim - 1
         counts = split_counts(global_spec.cells[axis], world) if world > 1 else [global_spec.cells[axis]]
         offset = sum(counts[:rank])
+        if transport not in ("nccl", "device", "host"):
+            raise ValueError(f"unknown halo transport {transport!r}")
         self.layout = SlabLayout(rank, world, axis, counts, offset, counts[rank],
-                                 boundary.is_periodic(axis))
+                                 boundary.is_periodic(axis), self_halo)
         self.dist = dist
         self.group = group
         self.transport = transport
@@ -118,7 +131,7 @@ class Slab:
         """Global (lo, hi) BC ids -> this rank's ids (HALO at inner faces)."""
         L = self.layout
         out = [tuple(p) for p in bc]
-        if L.world > 1:
+        if L.exchanges:
             lo, hi = out[L.axis]
             if L.lo_nbr is not None:
                 lo = BC_HALO
@@ -157,9 +170,25 @@ class Slab:
             raise ValueError("initial profile produced non-finite values")
         grid.interior()[...] = vals
 
+    @property
+    def device_resident(self) -> bool:
+        """The exchange and the max-allreduce run inside the library (so the
+        device controller's attempt graph can drive a slab run)."""
+        return self.transport == "device"
+
     def attach(self, dev) -> None:
         self.dev = dev
-        if self.transport == "nccl" and self.layout.world > 1:
+        L = self.layout
+        if self.transport == "device" and L.exchanges:
+            # one NCCL communicator owned by the library: rank 0 makes the id
+            from ._native import nccl_unique_id
+            uid = nccl_unique_id() if L.rank == 0 else None
+            if L.world > 1:
+                box = [uid]
+                self.dist.broadcast_object_list(box, src=0, group=self.group)
+                uid = box[0]
+            dev.attach_comm(uid, L.world, L.rank, L.lo_nbr, L.hi_nbr)
+        elif self.transport == "nccl" and L.world > 1:
             # one stream for kernels and NCCL: order is implicit
             dev.set_stream(_torch_stream())
 
@@ -192,10 +221,14 @@ class Slab:
         """Post the halo exchange of `buf`.  NCCL: the send/recv run on the
         collective stream behind the work already queued (the sweep that
         produced `buf`) and this returns at once; host transport: done on
-        return.  Pass the result to exchange_end."""
+        return; device transport: the library's exchange, on its stream.
+        Pass the result to exchange_end."""
         L = self.layout
-        if L.world == 1 or (L.lo_nbr is None and L.hi_nbr is None):
+        if not L.exchanges:
             return None
+        if self.transport == "device":
+            self.dev.halo_exchange(buf)
+            return ((), None)
         m = self.global_spec.num_states
         self._buf = buf
         sides = []
@@ -303,6 +336,9 @@ class Slab:
         """Sweeps of one attempt with the halo exchange overlapping the slow
         sweep; returns the max-allreduced per-sweep (speeds, nonfinite)."""
         dev = self.dev
+        if self.transport == "device":
+            # exchange, overlap and max-allreduce inside clb_attempt_step
+            return dev.attempt_step(dt, sim._cur, sim._scratch[0], sim._scratch[1])
         nd = len(sim.step_order)
         src = sim._cur
         for j in range(nd):

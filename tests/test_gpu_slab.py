@@ -90,3 +90,70 @@ def test_slab_on_device_is_bitwise_single_gpu(name, world):
         assert res[r][0] == ref_att
     glued = np.concatenate([res[r][1] for r in range(world)], axis=1)
     assert glued.tobytes() == ref.tobytes()
+
+
+# ---------------------------------------------------------------------------
+# The device-resident slab path (clb_attach_comm: NCCL inside the library,
+# the exchange and the max-allreduce inside the attempt graph).  One GPU, one
+# rank: a periodic slow axis is exchanged with the rank itself through NCCL
+# (lo/hi neighbour = rank 0, the slow-axis sides are HALO), which runs the
+# same pack -> ncclSend/ncclRecv -> unpack -> overlapped slow sweep ->
+# allreduce -> controller sequence as a multi-GPU run; the result must be
+# bit-identical to the single-domain periodic run.
+
+DEVICE_CASES = {
+    "sw_periodic": ("shallow_water2d", (96, 130), "gaussian_hump", {}, "periodic", "mc", 8,
+                    "float64"),
+    "sw_periodic_f32": ("shallow_water2d", (70, 203), "gaussian_hump", {}, "periodic",
+                        "superbee", 8, "float32"),
+    "ac3d_periodic": ("acoustics3d", (40, 33, 50), "gaussian_pressure", {"width": 0.2},
+                      "periodic", "mc", 5, "float64"),
+}
+
+
+def _device_recipe(name):
+    prob, cells, prof, opts, bc, lim, steps, dt = DEVICE_CASES[name]
+    nd = len(cells)
+    return dict(name=name, problem=prob, profile=prof, options=opts, cells=cells,
+                lower=(0.0,) * nd, upper=(1.0,) * nd, dtype=dt, bc=bc, limiter=lim,
+                speed="bound", drive=("max_steps", steps))
+
+
+@pytest.mark.parametrize("device_controller", [True, False], ids=["graph", "host-loop"])
+@pytest.mark.parametrize("name", sorted(DEVICE_CASES))
+def test_device_slab_exchange_with_itself_is_bitwise(name, device_controller):
+    r = _device_recipe(name)
+    ref_sim, _ = cases.product_sim(r)
+    with ref_sim:
+        ref_att = cases.attempts_hex(cases.drive(ref_sim, r))
+        ref = ref_sim.grid.interior().copy()
+    grid, params, problem, bspec, speed = cases.build_grid(r)
+    slab = Slab(grid.spec, bspec, 0, 1, None, transport="device", self_halo=True)
+    assert slab.layout.lo_nbr == 0 and slab.layout.hi_nbr == 0
+    with P.Simulation(grid, problem.solver, params, bspec, limiter=P.LimiterKind(r["limiter"]),
+                      initial_max_speed=speed, slab=slab,
+                      device_controller=device_controller) as sim:
+        att = cases.attempts_hex(cases.drive(sim, r))
+        assert att == ref_att
+        assert sim.grid.interior().tobytes() == ref.tobytes()
+
+
+def test_device_slab_blowup_location_through_the_exchange():
+    spec = P.GridSpec((40, 36), (0, 0), (1, 1), 3)
+    base = 0.05 * np.random.default_rng(3).standard_normal((3, 36, 40))
+    res = []
+    for use_slab in (False, True):
+        g = P.create_grid(spec)
+        g.interior()[...] = base
+        bspec = P.BoundarySpec.uniform(P.BoundaryKind.PERIODIC, (1, 2))
+        slab = Slab(spec, bspec, 0, 1, None, transport="device", self_halo=True) \
+            if use_slab else None
+        sim = P.Simulation(g, P.get_solver("acoustics"), P.AcousticsParams(), bspec,
+                           initial_max_speed=1.0, slab=slab)
+        sim.run_until(1e30, max_steps=2)
+        sim.grid.interior(0)[35, 7] = np.nan
+        with pytest.raises(P.NumericalBlowup) as exc:
+            sim.run_until(1e30, max_steps=3)
+        res.append((exc.value.state, exc.value.cell, exc.value.step))
+        sim.close()
+    assert res[0] == res[1]

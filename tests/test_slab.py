@@ -113,3 +113,20 @@ def test_decomposed_blowup_reports_global_first_cell():
     parts = _decomposed("sw_reflective", 2, nan_at)
     assert ref[0] == "blowup"
     assert all(p == ref for p in parts)
+
+
+def test_layout_neighbours_and_self_halo():
+    spec = P.GridSpec((8, 12), (0, 0), (1, 1), 3)
+    per = P.BoundarySpec.uniform(P.BoundaryKind.PERIODIC, (1, 2))
+    ref = P.BoundarySpec.uniform(P.BoundaryKind.REFLECTIVE, (1, 2))
+    s = Slab(spec, per, 0, 1, None, transport="device", self_halo=True)
+    assert (s.layout.lo_nbr, s.layout.hi_nbr, s.layout.exchanges) == (0, 0, True)
+    assert s.local_bc([(2, 2), (2, 2)])[1] == (3, 3) and s.device_resident
+    s = Slab(spec, per, 0, 1, None, transport="device")
+    assert (s.layout.lo_nbr, s.layout.hi_nbr, s.layout.exchanges) == (None, None, False)
+    s = Slab(spec, ref, 0, 1, None, transport="device", self_halo=True)
+    assert not s.layout.exchanges            # a reflective axis never wraps
+    s = Slab(spec, ref, 1, 3, None, transport="nccl")
+    assert (s.layout.lo_nbr, s.layout.hi_nbr) == (0, 2) and not s.device_resident
+    with pytest.raises(ValueError):
+        Slab(spec, ref, 0, 2, None, transport="carrier-pigeon")
