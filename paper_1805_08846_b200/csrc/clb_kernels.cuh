@@ -43,10 +43,27 @@ constexpr int kConsumers = 128;        // pencils per CTA
 #ifndef CLB_INLINE_PRODUCER
 #define CLB_INLINE_PRODUCER 0
 #endif
+#ifndef CLB_X_LEGACY
+#define CLB_X_LEGACY 0
+#endif
 // CLB_INLINE_PRODUCER: consumer thread 0 issues the stage copies (no
 // producer warp), so a CTA is 4 warps
 constexpr bool kInlineProducer = CLB_INLINE_PRODUCER != 0;
 constexpr int kThreads = kConsumers + (kInlineProducer ? 0 : 32);
+// The TMA x sweep issues its copies from consumer thread 0 by default: its
+// shared memory holds 3 CTAs per SM anyway, and without the producer warp
+// the same register file gives each thread 168 registers instead of 136
+// (the march spills less).  CLB_X_INLINE=0 restores the producer warp.
+#ifndef CLB_X_INLINE
+#define CLB_X_INLINE 1
+#endif
+constexpr bool kInlineX = CLB_X_INLINE != 0;
+template <bool CONTIG> constexpr bool inline_producer() {
+  return (CONTIG && !CLB_X_LEGACY) ? kInlineX : kInlineProducer;
+}
+template <bool CONTIG> constexpr int threads_of() {
+  return kConsumers + (inline_producer<CONTIG>() ? 0 : 32);
+}
 constexpr int kRowStrideContig = 48;   // bytes per row per state in a contig stage
 
 // Device-resident step controller state (clb_capi.cu ctl_* kernels; the
@@ -264,6 +281,7 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #define CLB_SW_MINB_X_INL 3
 #endif
 template <typename T, class S, bool CONTIG> constexpr int kMinBlocks() {
+  if (CONTIG && !CLB_X_LEGACY && kInlineX) return CLB_SW_MINB_X_INL;
   if (kInlineProducer)
     return (sizeof(T) == 8 && S::NW >= 3) ? (CONTIG ? CLB_SW_MINB_X_INL : CLB_SW_MINB_INL)
                                           : (sizeof(T) == 4 ? CLB_F32_MINB + 1 : CLB_F64_MINB + 1);
@@ -383,7 +401,8 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
                                              const T (&q2)[M]) {
     const bool e0 = same_bits<T, M>(q0, X[PP].q);
     const bool e1 = same_bits<T, M>(q1, q0), e2 = same_bits<T, M>(q2, q1);
-    const bool ok = idle || (run >= 2 && e0 && e1 && e2);
+    const bool eq = idle || (e0 && e1 && e2);
+    const bool ok = eq && (idle || run >= 2);
     run = e2 ? (e1 ? (e0 ? run + 3 : 2) : 1) : 0;
     if (__all_sync(FULL, ok) && (uni || __all_sync(FULL, idle || fan_finite(F[PP])))) {
       if (!uni) {
@@ -404,8 +423,12 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
       return true;
     }
     uni = false;
-    back = min(2 * back + 1, CLB_SKIP_BACKOFF);
-    cool = back;
+    // a uniform group that only lacked the run-up (run < 2, e.g. after
+    // unchecked groups) is checked again at once; anything else backs off
+    if (!__all_sync(FULL, eq)) {
+      back = min(2 * back + 1, CLB_SKIP_BACKOFF);
+      cool = back;
+    }
     return false;
   }
   // prologue steps (no output)
@@ -753,9 +776,6 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 #ifndef CLB_X_NSTAGE
 #define CLB_X_NSTAGE 3
 #endif
-#ifndef CLB_X_LEGACY
-#define CLB_X_LEGACY 0
-#endif
 template <typename T, class S> struct XGeom {
   static constexpr int NC = 64 / (int)sizeof(T);
   static constexpr int ROW = 64;                        // bytes per row per state
@@ -800,19 +820,19 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
     for (int q = 0; q < M; ++q)
       tma_load_4d(ring + s * G::BYTES + q * G::SBYTES, map_ld, cx, cy, cz, q, &full[s]);
   };
-  if (!kInlineProducer && warp == kConsumers / 32) {
+  if (!kInlineX && warp == kConsumers / 32) {
     if (lane == 0)
       for (int k = 0; k < nst; ++k) produce(k);
     return;
   }
-  if (kInlineProducer && tid == 0)
+  if (kInlineX && tid == 0)
     for (int k = 0; k < min(nst, NSTAGE); ++k) produce(k);
   // releases: stage k's slot goes back to the producer exactly once per pass
   int released = 0;                             // stages 0 .. released-1 are released
   auto release_upto = [&](int k) {              // thread 0 only
     for (; released < k; ++released) {
       mbar_arrive(&empty[slot(released)]);
-      if (kInlineProducer && released + NSTAGE < nst) produce(released + NSTAGE);
+      if (kInlineX && released + NSTAGE < nst) produce(released + NSTAGE);
     }
   };
 
@@ -860,8 +880,16 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
     }
     fence_proxy_async_smem();
   };
+  // the entered stage and the one before it (a fetch or an output is never
+  // older: outputs lag the inputs by two positions)
+  int entered = -1;
+  unsigned char* cur_st = ring;
+  unsigned char* prev_st = ring;
+  auto at = [&](int pos) {
+    return ((pos / NC) == entered ? cur_st : prev_st) + cell_off(pos & (NC - 1));
+  };
   auto fetch = [&](int r, T (&q)[M]) {
-    const unsigned char* st = stage_ptr(r / NC) + cell_off(r % NC);
+    const unsigned char* st = at(r);
 #pragma unroll
     for (int k = 0; k < M; ++k) q[k] = *reinterpret_cast<const T*>(st + k * G::SBYTES);
   };
@@ -883,7 +911,7 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
   };
   auto emit = [&](int e, const T (&o)[M]) {
     if (e < 0 || e >= len) return;              // (warp-uniform: e is)
-    unsigned char* st = stage_ptr(1 + e / NC) + cell_off(e % NC);
+    unsigned char* st = at(NC + e);
 #pragma unroll
     for (int q = 0; q < M; ++q) *reinterpret_cast<T*>(st + q * G::SBYTES) = o[q];
     if (active) {
@@ -893,12 +921,13 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
     if (e % NC == NC - 1 || e == len - 1) flush(1 + e / NC);
   };
   // stage transitions happen at positions r % NC == 0 (warp-uniform)
-  int entered = -1;
   auto need = [&](int r) {
     const int k = r / NC;
     if (k > entered) {
       enter(k);
       entered = k;
+      prev_st = cur_st;
+      cur_st = stage_ptr(k);
     }
   };
 
@@ -991,7 +1020,7 @@ __device__ __forceinline__ int segment_stages(const SweepArgs<T>& a) {
 // same TMA-issuing thread after bulk_wait), and its (smax, fin) replace pass
 // 1's.  Literal (blow-up) kernels run one ExactArith pass.
 template <typename T, class S, int LIM, bool LIT, bool CONTIG>
-__global__ void __launch_bounds__(kThreads, kMinBlocks<T, S, CONTIG>())
+__global__ void __launch_bounds__(threads_of<CONTIG>(), kMinBlocks<T, S, CONTIG>())
     sweep_kernel(const SweepArgs<T> a, const __grid_constant__ TmaMaps maps) {
   Live<T> L;
   if (!resolve_live(a, L)) return;
@@ -1359,13 +1388,14 @@ inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     configured.fetch_or(bit, std::memory_order_release);
   }
-  if (g.occ_out) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(g.occ_out, fn, kThreads,
+  if (g.occ_out) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(g.occ_out, fn,
+                                                                      threads_of<CONTIG>(),
                                                                       kSmem);
   SweepArgs<T> a = to_args<T>(g);
   static const TmaMaps none{};
   dim3 grid((unsigned)((g.n1 + kConsumers - 1) / kConsumers), (unsigned)(g.seg_end - g.seg_begin),
             (unsigned)g.n2);
-  fn<<<grid, kThreads, kSmem, st>>>(a, CONTIG ? *g.maps : none);
+  fn<<<grid, threads_of<CONTIG>(), kSmem, st>>>(a, CONTIG ? *g.maps : none);
   return cudaGetLastError();
 }
 
