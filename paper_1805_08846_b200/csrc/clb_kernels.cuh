@@ -320,6 +320,9 @@ template <typename T, class S, bool CONTIG> struct StageGeom {
 #ifndef CLB_UNIFORM_SKIP
 #define CLB_UNIFORM_SKIP 1
 #endif
+#ifndef CLB_STEP_REDO
+#define CLB_STEP_REDO 0
+#endif
 #ifndef CLB_SKIP_BACKOFF
 #define CLB_SKIP_BACKOFF 7   // most groups computed unchecked after failed checks
 #endif
@@ -438,11 +441,36 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
     cool = 0;
     back = 0;
   }
+  // CLB_STEP_REDO: a step (fan, correction, update) in which some lane left
+  // the FastArith domain is recomputed at once by the warp with ExactArith
+  // from the same inputs (the step only writes X[P], F[P], G[P-1] and its
+  // output), instead of the CTA re-running its whole segment.
+  static constexpr bool kStepRedo = CLB_STEP_REDO && D::template kBranchFree<T>;
+  template <int P, class D2> __device__ __forceinline__ void fan_raw(const T (&q)[M],
+                                                                     const SweepArgs<T>& a,
+                                                                     bool& b) {
+    constexpr int P1 = (P + 2) % 3;
+    X[P] = S::template make<D2>(q, b);
+    F[P] = S::template solve<D2>(X[P1], X[P], a.P, b);
+  }
+  template <int P, class D2> __device__ __forceinline__ void corr_raw(const SweepArgs<T>& a,
+                                                                      bool& b) {
+    constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
+    correction<S, LIT, D2, T>(F[P2], F[P1], F[P], a.P, dtdx, lim(a), G[P1], b);
+  }
+  __device__ __forceinline__ bool redo_due(bool sb) const { return __any_sync(FULL, sb && !idle); }
   template <int P> __device__ __forceinline__ void fan_body(const T (&q)[M],
                                                             const SweepArgs<T>& a, bool fold) {
-    constexpr int P1 = (P + 2) % 3;
-    X[P] = S::template make<D>(q, bad);
-    F[P] = S::template solve<D>(X[P1], X[P], a.P, bad);
+    if constexpr (kStepRedo) {
+      bool sb = false;
+      fan_raw<P, D>(q, a, sb);
+      if (redo_due(sb)) {
+        bool d = false;
+        fan_raw<P, ExactArith>(q, a, d);
+      }
+    } else {
+      fan_raw<P, D>(q, a, bad);
+    }
     if (fold) fold_speed<S, T>(F[P], a.P, smax);
   }
   template <int P> __device__ __forceinline__ void fan(const T (&q)[M], const SweepArgs<T>& a,
@@ -451,16 +479,36 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
   }
   template <int P> __device__ __forceinline__ void fan_corr(const T (&q)[M],
                                                             const SweepArgs<T>& a, bool fold) {
-    constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
     fan<P>(q, a, fold);
-    correction<S, LIT, D, T>(F[P2], F[P1], F[P], a.P, dtdx, lim(a), G[P1], bad);
+    if constexpr (kStepRedo) {
+      bool sb = false;
+      corr_raw<P, D>(a, sb);
+      if (redo_due(sb)) {
+        bool d = false;
+        corr_raw<P, ExactArith>(a, d);
+      }
+    } else {
+      corr_raw<P, D>(a, bad);
+    }
   }
   // steady step: returns the updated cell i-2 in `out`
   template <int P> __device__ __forceinline__ void step(const T (&q)[M], const SweepArgs<T>& a,
                                                         bool fold, T (&out)[M]) {
     constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3;
-    fan_body<P>(q, a, fold);
-    correction<S, LIT, D, T>(F[P2], F[P1], F[P], a.P, dtdx, lim(a), G[P1], bad);
+    if constexpr (kStepRedo) {
+      bool sb = false;
+      fan_raw<P, D>(q, a, sb);
+      corr_raw<P, D>(a, sb);
+      if (redo_due(sb)) {
+        bool d = false;
+        fan_raw<P, ExactArith>(q, a, d);
+        corr_raw<P, ExactArith>(a, d);
+      }
+      if (fold) fold_speed<S, T>(F[P], a.P, smax);
+    } else {
+      fan_body<P>(q, a, fold);
+      corr_raw<P, D>(a, bad);
+    }
     update<S, LIT, T>(X[P2].q, F[P2], F[P1], G[P1], G[P2], a.P, dtdx, out);
   }
 };
