@@ -289,6 +289,15 @@ template <typename T, class S, bool CONTIG> constexpr int kMinBlocks() {
                                         : (sizeof(T) == 4 ? CLB_F32_MINB : CLB_F64_MINB);
 }
 
+// Registers per thread that keep kMinBlocks CTAs resident (the whole 64K
+// register file, in 8-register units): given explicitly with __maxnreg__
+// because ptxas settles on 128 for __launch_bounds__(160, 3) where 136 fit
+// (the strided shallow-water sweep spills half as much at 136).
+template <typename T, class S, bool CONTIG> constexpr int reg_budget() {
+  const int r = (65536 / (threads_of<CONTIG>() * kMinBlocks<T, S, CONTIG>())) & ~7;
+  return r > 255 ? 255 : r;
+}
+
 template <typename T, class S, bool CONTIG> struct StageGeom {
   static constexpr int NC = CONTIG ? (kRowStrideContig / (int)sizeof(T)) : CLB_STRIDED_NC;  // cells/stage
   static constexpr int BYTES = CONTIG ? S::M * kConsumers * kRowStrideContig
@@ -321,7 +330,7 @@ template <typename T, class S, bool CONTIG> struct StageGeom {
 #define CLB_UNIFORM_SKIP 1
 #endif
 #ifndef CLB_STEP_REDO
-#define CLB_STEP_REDO 0
+#define CLB_STEP_REDO 1
 #endif
 #ifndef CLB_SKIP_BACKOFF
 #define CLB_SKIP_BACKOFF 7   // most groups computed unchecked after failed checks
@@ -441,10 +450,11 @@ template <typename T, class S, int LIM, bool LIT, class D> struct March {
     cool = 0;
     back = 0;
   }
-  // CLB_STEP_REDO: a step (fan, correction, update) in which some lane left
-  // the FastArith domain is recomputed at once by the warp with ExactArith
-  // from the same inputs (the step only writes X[P], F[P], G[P-1] and its
-  // output), instead of the CTA re-running its whole segment.
+  // CLB_STEP_REDO (default): a step (fan, correction, update) in which some
+  // lane left the FastArith domain is recomputed at once by the warp with
+  // ExactArith from the same inputs (the step only writes X[P], F[P], G[P-1]
+  // and its output), instead of the CTA re-running its whole segment
+  // (SW 8192^2 dam break 39.4 -> 47.2 Gcell-upd/s, profiles/r2_notes.md).
   static constexpr bool kStepRedo = CLB_STEP_REDO && D::template kBranchFree<T>;
   template <int P, class D2> __device__ __forceinline__ void fan_raw(const T (&q)[M],
                                                                      const SweepArgs<T>& a,
@@ -1068,7 +1078,7 @@ __device__ __forceinline__ int segment_stages(const SweepArgs<T>& a) {
 // same TMA-issuing thread after bulk_wait), and its (smax, fin) replace pass
 // 1's.  Literal (blow-up) kernels run one ExactArith pass.
 template <typename T, class S, int LIM, bool LIT, bool CONTIG>
-__global__ void __launch_bounds__(threads_of<CONTIG>(), kMinBlocks<T, S, CONTIG>())
+__global__ void __maxnreg__((reg_budget<T, S, CONTIG>()))
     sweep_kernel(const SweepArgs<T> a, const __grid_constant__ TmaMaps maps) {
   Live<T> L;
   if (!resolve_live(a, L)) return;
