@@ -176,12 +176,14 @@ bool make_tensor_map(clb_ctx* h, int buf, bool store, void* out) {
   // x stages: 64-byte rows (whole sectors) with the 64-byte swizzle
   // (clb_kernels.cuh XGeom); CLB_X_LEGACY: 48-byte rows, no swizzle
   const bool legacy = CLB_X_LEGACY != 0;
-  cuuint32_t box[4] = {(cuuint32_t)((legacy ? 48 : 64) / isz), 128u, 1u, 1u};
+  const int row = legacy ? 48 : clb::x_row_bytes(h->M);
+  cuuint32_t box[4] = {(cuuint32_t)(row / isz), 128u, 1u, 1u};
   cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
   CUresult r = enc((CUtensorMap*)out,
                    isz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                    h->buf[buf], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   legacy ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B,
+                   legacy ? CU_TENSOR_MAP_SWIZZLE_NONE
+                          : (row == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -260,7 +262,8 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
     pen_ctas = ((nx + 127) / 128) * g.n2;
   }
   // contig stages are 64 (legacy: 48) bytes of a row: segment starts stay aligned
-  const int64_t align = (axis == 0 && g.contig == 2) ? (CLB_X_LEGACY ? 48 : 64) / h->itemsize : 1;
+  const int64_t align =
+      (axis == 0 && g.contig == 2) ? (CLB_X_LEGACY ? 48 : clb::x_row_bytes(h->M)) / h->itemsize : 1;
   static const int64_t min_seg = [] {
     const char* e = getenv("CLB_MIN_SEG");
     return e ? std::max<int64_t>(4, atoll(e)) : (int64_t)16;

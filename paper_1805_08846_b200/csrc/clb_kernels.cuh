@@ -289,15 +289,10 @@ template <typename T, class S, bool CONTIG> constexpr int kMinBlocks() {
                                         : (sizeof(T) == 4 ? CLB_F32_MINB : CLB_F64_MINB);
 }
 
-// Registers per thread that keep kMinBlocks CTAs resident (the whole 64K
-// register file, in 8-register units): given explicitly with __maxnreg__
-// because ptxas settles on 128 for __launch_bounds__(160, 3) where 136 fit
-// (the strided shallow-water sweep spills half as much at 136).
-template <typename T, class S, bool CONTIG> constexpr int reg_budget() {
-  const int r = (65536 / (threads_of<CONTIG>() * kMinBlocks<T, S, CONTIG>())) & ~7;
-  return r > 255 ? 255 : r;
-}
-
+// (Register budgets come from __launch_bounds__: each SM sub-partition has
+// its own 16K-register file, so 3 CTAs of 5 warps -- 4 warps on some
+// sub-partitions -- get 128 registers, and an explicit __maxnreg__(136)
+// measured a whole CTA less resident per SM.)
 template <typename T, class S, bool CONTIG> struct StageGeom {
   static constexpr int NC = CONTIG ? (kRowStrideContig / (int)sizeof(T)) : CLB_STRIDED_NC;  // cells/stage
   static constexpr int BYTES = CONTIG ? S::M * kConsumers * kRowStrideContig
@@ -592,8 +587,9 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
       for (int k = 0; k < nst; ++k) produce(k);
     return;
   }
+  int issued = 0;   // inline producer: stages of this pass issued so far
   if (kInlineProducer && tid == 0)
-    for (int k = 0; k < min(nst, NSTAGE); ++k) produce(k);
+    for (; issued < min(nst, NSTAGE); ++issued) produce(issued);
   // ------------------------------ consumers ------------------------------
   const int t = tid;
   const bool active = t < nvalid;
@@ -748,8 +744,18 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   for (int k = 0; k < nst; ++k) {
     const int kk = k0 + k;
     const int s = kk % NSTAGE;
-    // inline producer: refill the slot stage k-1 used (stage k-1+NSTAGE)
-    if (kInlineProducer && t == 0 && k >= 1 && k - 1 + NSTAGE < nst) produce(k - 1 + NSTAGE);
+    // inline producer: issue every stage whose slot is already free (a
+    // non-blocking probe of its empty barrier), and block only for stage k
+    // itself -- thread 0 never waits for the other warps just to prefetch
+    if (kInlineProducer && t == 0) {
+      while (issued < nst && issued < k + NSTAGE) {
+        const int kq = k0 + issued;
+        if (issued > k && kq >= NSTAGE &&
+            !mbar_test_wait(&empty[kq % NSTAGE], ((kq / NSTAGE) - 1) & 1))
+          break;
+        produce(issued++);
+      }
+    }
     mbar_wait(&full[s], (kk / NSTAGE) & 1);
     unsigned char* st = smem + s * G::BYTES;
     patch(st, k);
@@ -832,14 +838,27 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 // back to global memory as one TMA store of the same box.  A stage's ring slot
 // is released to the producer when that store has finished reading it.
 #ifndef CLB_X_NSTAGE
-#define CLB_X_NSTAGE 3
+#define CLB_X_NSTAGE 0   // 0: from CLB_X_BUDGET
 #endif
+#ifndef CLB_X_ROW
+#define CLB_X_ROW 64    // box row bytes of the x stages for m <= 3 states (32 or 64)
+#endif
+#ifndef CLB_X_ROW4
+#define CLB_X_ROW4 64   // box row bytes of the x stages for m >= 4 states (32 or 64)
+#endif
+#ifndef CLB_X_BUDGET
+#define CLB_X_BUDGET (72 * 1024)   // shared memory of the stage ring (3 CTAs per SM)
+#endif
+// box row bytes of the x stages (host side: clb_capi.cu make_tensor_map)
+__host__ __device__ constexpr int x_row_bytes(int m) { return m >= 4 ? CLB_X_ROW4 : CLB_X_ROW; }
 template <typename T, class S> struct XGeom {
-  static constexpr int NC = 64 / (int)sizeof(T);
-  static constexpr int ROW = 64;                        // bytes per row per state
+  static constexpr int ROW = x_row_bytes(S::M);         // bytes per row per state
+  static constexpr int NC = ROW / (int)sizeof(T);
   static constexpr int SBYTES = kConsumers * ROW;       // one state of a stage
   static constexpr int BYTES = S::M * SBYTES;
-  static constexpr int NSTAGE = CLB_X_NSTAGE;
+  // as many stages as the ring budget holds (in-place outputs need >= 3)
+  static constexpr int NSTAGE_RAW = CLB_X_NSTAGE > 0 ? CLB_X_NSTAGE : CLB_X_BUDGET / BYTES;
+  static constexpr int NSTAGE = NSTAGE_RAW < 3 ? 3 : (NSTAGE_RAW > 8 ? 8 : NSTAGE_RAW);
   static constexpr int SMEM = NSTAGE * BYTES + 2 * NSTAGE * 8 + 1024;  // + 1024-B alignment slack
 };
 
@@ -900,7 +919,9 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
   const bool halo_lo = a.bc_lo == BC_HALO, halo_hi = a.bc_hi == BC_HALO;
   // swizzled byte offset of (row t, cell c) inside one state's box
   const int rowb = t * G::ROW;
-  const int xr = ((t >> 1) & 3) << 4;
+  // 64-byte swizzle: 16-byte chunk ^= (offset >> 7) & 3, i.e. (t >> 1) & 3;
+  // 32-byte swizzle: chunk ^= (offset >> 7) & 1, i.e. (t >> 2) & 1
+  const int xr = G::ROW == 64 ? ((t >> 1) & 3) << 4 : ((t >> 2) & 1) << 4;
   auto cell_off = [&](int c) { return rowb + ((c * isz) ^ xr); };
 
   March<T, S, LIM, LIT, D> mr;
@@ -1078,7 +1099,7 @@ __device__ __forceinline__ int segment_stages(const SweepArgs<T>& a) {
 // same TMA-issuing thread after bulk_wait), and its (smax, fin) replace pass
 // 1's.  Literal (blow-up) kernels run one ExactArith pass.
 template <typename T, class S, int LIM, bool LIT, bool CONTIG>
-__global__ void __maxnreg__((reg_budget<T, S, CONTIG>()))
+__global__ void __launch_bounds__(threads_of<CONTIG>(), kMinBlocks<T, S, CONTIG>())
     sweep_kernel(const SweepArgs<T> a, const __grid_constant__ TmaMaps maps) {
   Live<T> L;
   if (!resolve_live(a, L)) return;
