@@ -152,6 +152,21 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
+// L2 promotion of the x boxes (CLB_TMA_PROMO = none|64|128|256; 128 default)
+CUtensorMapL2promotion tma_promotion() {
+  static const CUtensorMapL2promotion p = [] {
+    const char* e = getenv("CLB_TMA_PROMO");
+    if (!e) return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    switch (atoi(e)) {
+      case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+      case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+      case 256: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+      default: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    }
+  }();
+  return p;
+}
+
 // 4-D view (x, y, z, state) of one buffer for the contiguous-axis sweep: box =
 // 48 bytes of x by 128 rows.  `store` limits the extent to the interior so
 // tiles that overhang the grid are clipped by the TMA unit.
@@ -184,7 +199,7 @@ bool make_tensor_map(clb_ctx* h, int buf, bool store, void* out) {
                    h->buf[buf], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    legacy ? CU_TENSOR_MAP_SWIZZLE_NONE
                           : (row == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   tma_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -236,9 +251,13 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   // blocks for the TMA variant and run faster warp-marching (56 vs 69 us).
   // clb_set_x_variant (per handle) overrides.
   const int64_t ncells = h->cells[0] * h->cells[1] * h->cells[2];
+  // 3-D acoustics (m = 4) also streams x faster through the TMA transpose
+  // with 32-byte rows on large grids (C5 fp64 x 2.20 vs 2.39 ms, r2j)
+  const bool big = ncells >= ((int64_t)1 << 22);
   const int contig_mode = h->x_variant ? h->x_variant
-                          : ((h->d.solver_id == CLB_SOLVER_SHALLOW_WATER &&
-                              ncells >= ((int64_t)1 << 22)) ? 2 : 1);
+                          : (big && (h->d.solver_id == CLB_SOLVER_SHALLOW_WATER ||
+                                     (h->d.solver_id == CLB_SOLVER_ACOUSTICS && h->ndim == 3)))
+                                ? 2 : 1;
   if (axis == 0) {
     g.contig = (contig_mode == 2 && h->have_maps) ? 2 : 1;
     g.n = (int)nx; g.n1 = (int)ny; g.n2 = (int)nz;
@@ -723,6 +742,12 @@ int clb_create(const clb_desc* desc, clb_handle* out) {
   // slack past the x ghosts: contig stages may read up to 16 cells beyond n
   // (beyond the row the TMA unit zero-fills)
   h->px = (h->xoff + h->cells[0] + 16 + align - 1) / align * align;
+  {
+    // CLB_PITCH_PAD: extra 128-byte units per row (layout experiments; results
+    // are independent of the pitch)
+    const char* e = getenv("CLB_PITCH_PAD");
+    if (e) h->px += std::max(0, atoi(e)) * align;
+  }
   h->ypad = d.ndim >= 2 ? h->cells[1] + 4 : 1;
   h->zpad = d.ndim == 3 ? h->cells[2] + 4 : 1;
   h->ystride = h->px;

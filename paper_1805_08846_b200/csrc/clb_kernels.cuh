@@ -837,6 +837,12 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 // cell (read two steps earlier by the same thread) and each stage >= 1 goes
 // back to global memory as one TMA store of the same box.  A stage's ring slot
 // is released to the producer when that store has finished reading it.
+#ifndef CLB_DIAG_NOSTORE
+#define CLB_DIAG_NOSTORE 0
+#endif
+#if defined(CLB_DEFAULT_LIB) && CLB_DIAG_NOSTORE
+#error "CLB_DIAG_NOSTORE is timing-only and not allowed in the default library"
+#endif
 #ifndef CLB_X_NSTAGE
 #define CLB_X_NSTAGE 0   // 0: from CLB_X_BUDGET
 #endif
@@ -844,7 +850,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 #define CLB_X_ROW 64    // box row bytes of the x stages for m <= 3 states (32 or 64)
 #endif
 #ifndef CLB_X_ROW4
-#define CLB_X_ROW4 64   // box row bytes of the x stages for m >= 4 states (32 or 64)
+#define CLB_X_ROW4 32   // box row bytes of the x stages for m >= 4 states (32 or 64)
 #endif
 #ifndef CLB_X_BUDGET
 #define CLB_X_BUDGET (72 * 1024)   // shared memory of the stage ring (3 CTAs per SM)
@@ -979,8 +985,10 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
     if (t == 0) {
       const unsigned char* st = stage_ptr(k);
       const int cx = a.tx0 + lo + (k - 1) * NC;
+      if (!CLB_DIAG_NOSTORE) {  // timing experiments only: outputs discarded
 #pragma unroll
-      for (int q = 0; q < M; ++q) tma_store_4d(map_st, st + q * G::SBYTES, cx, cy, cz, q);
+        for (int q = 0; q < M; ++q) tma_store_4d(map_st, st + q * G::SBYTES, cx, cy, cz, q);
+      }
       bulk_commit();
       // every stage before k is consumed; the store of k-1 has read its slot
       // once at most this newest group is still reading

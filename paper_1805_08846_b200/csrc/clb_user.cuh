@@ -24,6 +24,8 @@ template <typename T, int M_, int N_, int NW_, class U> struct ScalarSolver {
   static constexpr bool kDataSpeeds = true;
   // a user routine may return nonzero waves for equal states
   static constexpr bool kUniformSkip = false;
+  static constexpr bool kSignedSpeeds = false;
+  __host__ __device__ static constexpr int speed_sign(int) { return 0; }
   struct Cell { T q[M]; };
   struct Fan { T W[NW][M]; T s[NW]; };
   template <class D = ExactArith>
