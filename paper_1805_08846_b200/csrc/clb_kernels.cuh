@@ -277,11 +277,15 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #ifndef CLB_SW_MINB_INL
 #define CLB_SW_MINB_INL 4
 #endif
+#ifndef CLB_X_MINB
+#define CLB_X_MINB 3   // resident CTAs of the TMA x sweep of the other solvers
+#endif
 #ifndef CLB_SW_MINB_X_INL
 #define CLB_SW_MINB_X_INL 3
 #endif
 template <typename T, class S, bool CONTIG> constexpr int kMinBlocks() {
-  if (CONTIG && !CLB_X_LEGACY && kInlineX) return CLB_SW_MINB_X_INL;
+  if (CONTIG && !CLB_X_LEGACY && kInlineX)
+    return (sizeof(T) == 8 && S::NW >= 3) ? CLB_SW_MINB_X_INL : CLB_X_MINB;
   if (kInlineProducer)
     return (sizeof(T) == 8 && S::NW >= 3) ? (CONTIG ? CLB_SW_MINB_X_INL : CLB_SW_MINB_INL)
                                           : (sizeof(T) == 4 ? CLB_F32_MINB + 1 : CLB_F64_MINB + 1);
@@ -853,7 +857,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 #define CLB_X_ROW4 32   // box row bytes of the x stages for m >= 4 states (32 or 64)
 #endif
 #ifndef CLB_X_BUDGET
-#define CLB_X_BUDGET (72 * 1024)   // shared memory of the stage ring (3 CTAs per SM)
+#define CLB_X_BUDGET 0   // stage-ring bytes; 0: the share of the resident CTAs
 #endif
 // box row bytes of the x stages (host side: clb_capi.cu make_tensor_map)
 __host__ __device__ constexpr int x_row_bytes(int m) { return m >= 4 ? CLB_X_ROW4 : CLB_X_ROW; }
@@ -863,7 +867,10 @@ template <typename T, class S> struct XGeom {
   static constexpr int SBYTES = kConsumers * ROW;       // one state of a stage
   static constexpr int BYTES = S::M * SBYTES;
   // as many stages as the ring budget holds (in-place outputs need >= 3)
-  static constexpr int NSTAGE_RAW = CLB_X_NSTAGE > 0 ? CLB_X_NSTAGE : CLB_X_BUDGET / BYTES;
+  // the resident CTAs' share of the 228 KB (less static + reserved memory)
+  static constexpr int BUDGET =
+      CLB_X_BUDGET > 0 ? CLB_X_BUDGET : (228 * 1024) / kMinBlocks<T, S, true>() - 3 * 1024;
+  static constexpr int NSTAGE_RAW = CLB_X_NSTAGE > 0 ? CLB_X_NSTAGE : BUDGET / BYTES;
   static constexpr int NSTAGE = NSTAGE_RAW < 3 ? 3 : (NSTAGE_RAW > 8 ? 8 : NSTAGE_RAW);
   static constexpr int SMEM = NSTAGE * BYTES + 2 * NSTAGE * 8 + 1024;  // + 1024-B alignment slack
 };
