@@ -328,6 +328,10 @@ def run_gpu(args, rank, world, scaling):
         else:
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = tdist
+        import logging
+        logging.basicConfig(level=logging.WARNING, stream=sys.stderr,
+                            format="[rank %d] %%(name)s: %%(message)s" % rank)
+        logging.getLogger("clawtile.slab").setLevel(logging.INFO)
     gcells = global_cells(args.workload, world, scaling)
     inp = build_inputs(args.workload, gcells, world, rank, dist, args.transport)
     P = inp["P"]

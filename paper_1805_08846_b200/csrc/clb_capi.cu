@@ -1386,10 +1386,11 @@ extern "C" int clb_attach_comm(clb_handle h, const void* id, int nranks, int ran
   h->halo_recv_off[0] = (const char*)recv_lo - b0;
   h->halo_recv_off[1] = (const char*)recv_hi - b0;
   h->halo_block = bb;
-  CLB_CUDA(h, cudaMalloc(&h->halo_stage, 4 * (size_t)h->M * bb));
-  CLB_CUDA(h, cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
-  CLB_CUDA(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
-  CLB_CUDA(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  // (a failed earlier attach may have left these behind)
+  if (!h->halo_stage) CLB_CUDA(h, cudaMalloc(&h->halo_stage, 4 * (size_t)h->M * bb));
+  if (!h->side) CLB_CUDA(h, cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  if (!h->ev_fork) CLB_CUDA(h, cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  if (!h->ev_join) CLB_CUDA(h, cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
   ncclComm_t comm = nullptr;

@@ -31,12 +31,15 @@ the CPU (gloo) tests and the single-GPU multi-process test use.
 
 from __future__ import annotations
 
+import logging
 from dataclasses import dataclass
 
 import numpy as np
 
 from .boundary import BC_HALO
 from .grid import GridSpec, StateGrid
+
+log = logging.getLogger("clawtile.slab")
 
 
 def split_counts(n: int, parts: int) -> list[int]:
@@ -188,6 +191,10 @@ class Slab:
                 self.dist.broadcast_object_list(box, src=0, group=self.group)
                 uid = box[0]
             dev.attach_comm(uid, L.world, L.rank, L.lo_nbr, L.hi_nbr)
+            # visible in the job log: one line per rank once the communicator exists
+            log.info("clb NCCL communicator ready: rank %d of %d, slow axis %d, neighbours "
+                     "lo=%s hi=%s, owned %d of %d cells", L.rank, L.world, L.axis, L.lo_nbr,
+                     L.hi_nbr, L.count, self.global_spec.cells[L.axis])
         elif self.transport == "nccl" and L.world > 1:
             # one stream for kernels and NCCL: order is implicit
             dev.set_stream(_torch_stream())
