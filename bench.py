@@ -72,6 +72,9 @@ WORKLOADS = {
     "sw8192": ("shallow_water2d", (8192, 8192), (-1, -1), (1, 1), "radial_dam_break", {},
                "reflective", "mc", "double",
                "north-star: 2D shallow water 8192^2 radial dam-break, fp64"),
+    "c4lake": ("shallow_water2d", (16384, 16384), (-1, -1), (1, 1), "lake_at_rest", {},
+               "reflective", "mc", "double",
+               "SW 16384^2 lake at rest (every cell uniform: the sweeps' pure streaming limit), fp64"),
     "sw8192hump": ("shallow_water2d", (8192, 8192), (0, 0), (1, 1), "gaussian_hump", {},
                    "reflective", "mc", "double",
                    "2D shallow water 8192^2 gaussian hump (flow active in every cell), fp64"),

@@ -679,7 +679,8 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   };
   // emit the updated cell e = r - A - 4 of the segment (cell lo + e).  Contig
   // sweeps stage it in output tile e / NC (double-buffered) for a TMA store.
-  auto emit = [&](int r, bool valid, const T (&o)[M]) {
+  // fold = false: the outputs are known finite (a skipped group)
+  auto emit = [&](int r, bool valid, const T (&o)[M], bool fold = true) {
     if (CONTIG) {
       const int e = r - A - 4;
       unsigned char* ob = outs + ((e / NC) & 1) * G::BYTES;
@@ -687,7 +688,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
       for (int q = 0; q < M; ++q)
         *reinterpret_cast<T*>(ob + (q * kConsumers + t) * kRowStrideContig +
                               (e % NC) * (int)sizeof(T)) = o[q];
-      if (valid && active) {
+      if (fold && valid && active) {
 #pragma unroll
         for (int q = 0; q < M; ++q) mr.fin = min(mr.fin, finite_key(o[q]));
       }
@@ -696,7 +697,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
       T* ob = reinterpret_cast<T*>(outs + ((e / NC) & 1) * G::BYTES);
 #pragma unroll
       for (int q = 0; q < M; ++q) ob[(q * NC + e % NC) * kConsumers + t] = o[q];
-      if (valid && active) {
+      if (fold && valid && active) {
 #pragma unroll
         for (int q = 0; q < M; ++q) mr.fin = min(mr.fin, finite_key(o[q]));
       }
@@ -705,7 +706,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 #pragma unroll
       for (int q = 0; q < M; ++q) {
         dst[q * a.sstride] = o[q];
-        mr.fin = min(mr.fin, finite_key(o[q]));
+        if (fold) mr.fin = min(mr.fin, finite_key(o[q]));
       }
     }
   };
@@ -776,9 +777,10 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
           fetch(st, c0 + 1, q1);
           fetch(st, c0 + 2, q2);
           if (mr.template skip_group<2>(q, q1, q2)) {
-            emit(r0, r0 < ncell, q);
-            emit(r0 + 1, r0 + 1 < ncell, q1);
-            emit(r0 + 2, r0 + 2 < ncell, q2);
+            // (finite: a skip needs a finite fan, so no finiteness fold)
+            emit(r0, r0 < ncell, q, false);
+            emit(r0 + 1, r0 + 1 < ncell, q1, false);
+            emit(r0 + 2, r0 + 2 < ncell, q2, false);
             if ((CONTIG || (G::NOUT > 0 && bulk_out)) && (r0 + 2 - A - 4) % NC == NC - 1)
               flush((r0 + 2 - A - 4) / NC);
             continue;
@@ -1006,12 +1008,23 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
   auto emit = [&](int e, const T (&o)[M]) {
     if (e < 0 || e >= len) return;              // (warp-uniform: e is)
     unsigned char* st = at(NC + e);
+    // a state no wave touches leaves the update as its input bits (update():
+    // out = q), which the in-place slot already holds
 #pragma unroll
-    for (int q = 0; q < M; ++q) *reinterpret_cast<T*>(st + q * G::SBYTES) = o[q];
+    for (int q = 0; q < M; ++q)
+      if (LIT || !allzero<S>(q)) *reinterpret_cast<T*>(st + q * G::SBYTES) = o[q];
     if (active) {
 #pragma unroll
       for (int q = 0; q < M; ++q) mr.fin = min(mr.fin, finite_key(o[q]));
     }
+    if (e % NC == NC - 1 || e == len - 1) flush(1 + e / NC);
+  };
+  // a skipped group's outputs equal its inputs, which already sit in the
+  // output slots (in place: slot NC + e still holds cell e's input, equal to
+  // the uniform state) and are finite (a skip needs a finite fan, and a
+  // non-finite state makes its fans non-finite): nothing to write
+  auto emit_same = [&](int e) {
+    if (e < 0 || e >= len) return;
     if (e % NC == NC - 1 || e == len - 1) flush(1 + e / NC);
   };
   // stage transitions happen at positions r % NC == 0 (warp-uniform)
@@ -1056,9 +1069,9 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
         need(r + 2);
         fetch(r + 2, q2);
         if (mr.template skip_group<(P0 + 2) % 3>(q, q1, q2)) {
-          emit(r - NC - 2, q);
-          emit(r - NC - 1, q1);
-          emit(r - NC, q2);
+          emit_same(r - NC - 2);
+          emit_same(r - NC - 1);
+          emit_same(r - NC);
           continue;
         }
         mr.uni = false;
