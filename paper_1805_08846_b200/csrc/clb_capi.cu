@@ -198,7 +198,8 @@ bool make_tensor_map(clb_ctx* h, int buf, bool store, void* out) {
                    isz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                    h->buf[buf], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    legacy ? CU_TENSOR_MAP_SWIZZLE_NONE
-                          : (row == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
+                          : (row == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                             : row == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
                    tma_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

@@ -936,7 +936,9 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
   const int rowb = t * G::ROW;
   // 64-byte swizzle: 16-byte chunk ^= (offset >> 7) & 3, i.e. (t >> 1) & 3;
   // 32-byte swizzle: chunk ^= (offset >> 7) & 1, i.e. (t >> 2) & 1
-  const int xr = G::ROW == 64 ? ((t >> 1) & 3) << 4 : ((t >> 2) & 1) << 4;
+  // (128-byte rows, 128-byte swizzle: chunk ^= t & 7)
+  const int xr = G::ROW == 128 ? (t & 7) << 4
+                 : G::ROW == 64 ? ((t >> 1) & 3) << 4 : ((t >> 2) & 1) << 4;
   auto cell_off = [&](int c) { return rowb + ((c * isz) ^ xr); };
 
   March<T, S, LIM, LIT, D> mr;
