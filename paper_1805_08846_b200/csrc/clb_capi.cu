@@ -58,7 +58,7 @@ struct clb_ctx {
   int num_sms = 148;
   int seg_override[3] = {0, 0, 0};
   int x_variant = 0;        // CLB_XVAR_*: 0 = automatic
-  int resident[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // [axis][contig mode]: CTAs per SM
+  int resident[3][4] = {};  // [axis][contig mode]: CTAs per SM
   clb::TmaMaps maps;        // per buffer: load map, store map
   // device-resident controller (clb_run_batch)
   clb::DevCtl* d_ctl = nullptr;
@@ -260,7 +260,7 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
                                      (h->d.solver_id == CLB_SOLVER_ACOUSTICS && h->ndim == 3)))
                                 ? 2 : 1;
   if (axis == 0) {
-    g.contig = (contig_mode == 2 && h->have_maps) ? 2 : 1;
+    g.contig = contig_mode == 2 ? (h->have_maps ? 2 : 1) : contig_mode;
     g.n = (int)nx; g.n1 = (int)ny; g.n2 = (int)nz;
     g.astride = 1; g.t1stride = h->ystride; g.t2stride = h->zstride;
     g.maps = &h->maps;
@@ -269,7 +269,7 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
     g.tz0 = h->ndim == 3 ? 2 : 0;
     // warp-marching: one warp per (row, segment), 4 warps per CTA;
     // TMA: 128 rows of one z-plane per CTA
-    pen_ctas = g.contig == 1 ? (ny * nz + 3) / 4 : ((ny + 127) / 128) * nz;
+    pen_ctas = g.contig != 2 ? (ny * nz + 3) / 4 : ((ny + 127) / 128) * nz;
   } else {
     g.contig = 0;
     g.n1 = (int)nx;
@@ -293,11 +293,13 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   auto seg_len_of = [&](int64_t ns) {
     int64_t L = (g.n + ns - 1) / ns;
     if (axis == 0 && g.contig == 1) L = std::max<int64_t>(28, (L + 4 + 31) / 32 * 32 - 4);
+    // pair march: 64-cell chunks from lo - 4 while b - 2 < hi, i.e. L + 2 of 64
+    if (axis == 0 && g.contig == 3) L = std::max<int64_t>(62, (L + 2 + 63) / 64 * 64 - 2);
     return (L + align - 1) / align * align;
   };
   // CTAs a segment count launches (the warp-march packs 4 row-warps per CTA)
   auto ctas_of = [&](int64_t ns) {
-    return (axis == 0 && g.contig == 1) ? (ny * nz * ns + 3) / 4 : pen_ctas * ns;
+    return (axis == 0 && g.contig != 2) ? (ny * nz * ns + 3) / 4 : pen_ctas * ns;
   };
   // Segment count: maximise (busy fraction of the last wave) x (L / (L+4),
   // the share of non-redundant work) over the resident CTA slots, so that
@@ -836,7 +838,8 @@ int clb_set_segments(clb_handle h, int axis, int seg_len) {
 
 int clb_set_x_variant(clb_handle h, int variant) {
   if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
-  if (variant < CLB_XVAR_AUTO || variant > CLB_XVAR_TMA) return fail(h, CLB_EINVAL, "unknown x-sweep variant");
+  if (variant < CLB_XVAR_AUTO || variant > CLB_XVAR_PAIR)
+    return fail(h, CLB_EINVAL, "unknown x-sweep variant");
   if (variant == CLB_XVAR_TMA && !h->have_maps)
     return fail(h, CLB_EUNSUPPORTED, "TMA tensor maps unavailable on this device");
   h->x_variant = variant;

@@ -1394,6 +1394,211 @@ __global__ void __launch_bounds__(128, CLB_CONTIG_MINB) sweep_contig(const Sweep
 }
 
 // ---------------------------------------------------------------------------
+// Axis 0 (contiguous): pair warp-march.  A warp marches along one row in
+// 64-cell chunks, lane l owning cells x0 = b + 2l and x1 = x0 + 1.  Per lane
+// and chunk: the fans F(x0) (left neighbour = lane l-1's second cell) and
+// F(x1), the corrections G(x0-1) and G(x0), and the updates of cells x0-2
+// and x0-1 (lane l-1's pair).  Lane l-1's second cell, its two fans and its
+// G(x0-2) arrive by __shfl_up (lane 0 from the previous chunk's lane 31
+// through a per-warp shared-memory carry), and the two output cells' states
+// are read from the staged chunk: half the shuffles per cell of
+// sweep_contig.  Loads: the next chunk streams into a per-warp shared buffer
+// with per-thread cp.async (two consecutive cells per lane per state).
+template <typename T, class S> struct PairCarry {
+  static constexpr int kCell = (int)(sizeof(typename S::Cell) / sizeof(T));
+  static constexpr int kFan = (int)(sizeof(typename S::Fan) / sizeof(T));
+  // cell c1, fans Fa, Fb, correction Ga, states q0, q1 of the last lane
+  static constexpr int kAll = kCell + 2 * kFan + 3 * S::M;
+};
+
+template <typename T, class S, bool LIT, class D>
+__device__ __forceinline__ void pair_chunk(const SweepArgs<T>& a, T dtdx, int lim_id,
+                                           const T (&q0)[S::M], const T (&q1)[S::M],
+                                           bool first, int lane, const T* carry,
+                                           typename S::Fan& Fa, typename S::Fan& Fb,
+                                           typename S::Cell& c1, T (&Ga)[S::M],
+                                           T (&oA)[S::M], T (&oB)[S::M],
+                                           const T (&pq0)[S::M], const T (&pq1)[S::M],
+                                           bool& bad) {
+  using Cell = typename S::Cell;
+  using Fan = typename S::Fan;
+  constexpr int M = S::M;
+  constexpr int KC = PairCarry<T, S>::kCell, KF = PairCarry<T, S>::kFan;
+  const Cell c0 = S::template make<D>(q0, bad);
+  c1 = S::template make<D>(q1, bad);
+  const bool from_carry = lane == 0 && !first;
+  Cell cL = c1;
+  S::for_cell_regs(cL, [&](T& r) { r = __shfl_up_sync(FULL, r, 1); });
+  if (from_carry) {
+    int i = 0;
+    S::for_cell_regs(cL, [&](T& r) { r = carry[i++]; });
+  }
+  Fa = S::template solve<D>(cL, c0, a.P, bad);     // F(x0)
+  Fb = S::template solve<D>(c0, c1, a.P, bad);     // F(x1)
+  Fan Fpa = Fa, Fpb = Fb;                          // lane l-1's F(x0-2), F(x0-1)
+  S::for_regs(Fpa, [&](T& r) { r = __shfl_up_sync(FULL, r, 1); });
+  S::for_regs(Fpb, [&](T& r) { r = __shfl_up_sync(FULL, r, 1); });
+  if (from_carry) {
+    int i = KC;
+    S::for_regs(Fpa, [&](T& r) { r = carry[i++]; });
+    S::for_regs(Fpb, [&](T& r) { r = carry[i++]; });
+  }
+  T Gm[M];
+  correction<S, LIT, D, T>(Fpa, Fpb, Fa, a.P, dtdx, lim_id, Gm, bad);   // G(x0-1)
+  correction<S, LIT, D, T>(Fpb, Fa, Fb, a.P, dtdx, lim_id, Ga, bad);    // G(x0)
+  T Gl[M];                                                              // G(x0-2)
+#pragma unroll
+  for (int k = 0; k < M; ++k) Gl[k] = __shfl_up_sync(FULL, Ga[k], 1);
+  if (from_carry) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) Gl[k] = carry[KC + 2 * KF + k];
+  }
+  update<S, LIT, T>(pq0, Fpa, Fpb, Gm, Gl, a.P, dtdx, oA);   // cell x0-2
+  update<S, LIT, T>(pq1, Fpb, Fa, Ga, Gm, a.P, dtdx, oB);    // cell x0-1
+}
+
+#ifndef CLB_PAIR_MINB
+#define CLB_PAIR_MINB 2
+#endif
+template <typename T, class S, int LIM, bool LIT>
+__global__ void __launch_bounds__(128, CLB_PAIR_MINB) sweep_pair(const SweepArgs<T> a) {
+  Live<T> L;
+  if (!resolve_live(a, L)) return;
+  const int lim_id = LIM >= 0 ? LIM : a.lim_id;
+  using Cell = typename S::Cell;
+  using Fan = typename S::Fan;
+  constexpr int M = S::M;
+  constexpr int KC = PairCarry<T, S>::kCell, KF = PairCarry<T, S>::kFan;
+  constexpr int KA = PairCarry<T, S>::kAll;
+  __shared__ T carry[4][KA];
+  // per warp: the chunk being marched and the next one (64 cells per state)
+  __shared__ T stage[4][2][M][64];
+
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nrows = (int64_t)a.n1 * a.n2;
+  const int64_t row = gw / a.nseg;
+  const int seg = (int)(gw - row * a.nseg);
+
+  T smax = T(0);
+  uint32_t fin = 0xffffffffu;
+  if (row < nrows) {
+    const int y = (int)(row % a.n1);
+    const int z = (int)(row / a.n1);
+    const int64_t off = (int64_t)y * a.t1stride + (int64_t)z * a.t2stride;
+    const T* qrow = L.qin + off;
+    T* orow = L.qout + off;
+    const int lo = seg * a.seg_len;
+    const int hi = min(a.n, lo + a.seg_len);
+    // chunk cells b .. b+63 (cells past hi+1 are never used); ghosts remapped
+    // at issue, the reflective negation applied at read
+    auto issue = [&](int bb, int buf) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int x = bb + 2 * lane + h;
+        int js = min(x, hi + 1);
+        if (!(bb >= 0 && bb + 63 < a.n)) {
+          bool neg;
+          js = remap(js, a.n, a.bc_lo, a.bc_hi, neg);
+        }
+        const T* p = qrow + js;
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          cp_async<(int)sizeof(T)>(&stage[wib][buf][k][2 * lane + h], p + k * a.sstride);
+      }
+      cp_async_commit();
+    };
+    auto read = [&](int bb, int buf, int idx, T (&q)[M]) {
+      bool neg = false;
+      if (!(bb >= 0 && bb + 63 < a.n)) remap(min(bb + idx, hi + 1), a.n, a.bc_lo, a.bc_hi, neg);
+#pragma unroll
+      for (int k = 0; k < M; ++k) q[k] = neg_if(stage[wib][buf][k][idx], neg && k == a.nv);
+    };
+    const int b0 = lo - 4;
+    issue(b0, 0);
+    int cur = 0;
+    for (int b = b0; b - 2 < hi; b += 64) {
+      const bool first = b == b0;
+      if (b + 64 - 2 < hi) issue(b + 64, cur ^ 1);
+      else cp_async_commit();
+      cp_async_wait<1>();
+      __syncwarp();
+      const int x0 = b + 2 * lane;
+      T q0[M], q1[M], pq0[M], pq1[M];
+      read(b, cur, 2 * lane, q0);
+      read(b, cur, 2 * lane + 1, q1);
+      // the two output cells (lane l-1's pair): the staged chunk, or the
+      // carry for lane 0
+      if (lane > 0) {
+        read(b, cur, 2 * lane - 2, pq0);
+        read(b, cur, 2 * lane - 1, pq1);
+      } else {
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          pq0[k] = carry[wib][KC + 2 * KF + M + k];
+          pq1[k] = carry[wib][KC + 2 * KF + 2 * M + k];
+        }
+      }
+      Fan Fa, Fb;
+      Cell c1;
+      T Ga[M], oA[M], oB[M];
+      bool bad = false;
+      if (LIT || (sizeof(T) == 4 && !CLB_CONTIG_FAST32)) {
+        pair_chunk<T, S, LIT, ExactArith>(a, L.dtdx, lim_id, q0, q1, first, lane, carry[wib], Fa,
+                                          Fb, c1, Ga, oA, oB, pq0, pq1, bad);
+      } else {
+        pair_chunk<T, S, LIT, FastArith>(a, L.dtdx, lim_id, q0, q1, first, lane, carry[wib], Fa,
+                                         Fb, c1, Ga, oA, oB, pq0, pq1, bad);
+        // the chunk is a pure function of its loads and the carry: recompute
+        // it exactly when a real lane left the fast-path domain
+        if (__any_sync(FULL, bad && x0 >= lo - 2 && x0 <= hi + 1)) {
+          bad = false;
+          pair_chunk<T, S, LIT, ExactArith>(a, L.dtdx, lim_id, q0, q1, first, lane, carry[wib],
+                                            Fa, Fb, c1, Ga, oA, oB, pq0, pq1, bad);
+        }
+      }
+      // commit: max |s| of the fans in [lo-1, hi+1], the outputs in [lo, hi)
+      if (x0 >= lo - 1 && x0 <= hi + 1) fold_speed<S, T>(Fa, a.P, smax);
+      if (x0 + 1 >= lo - 1 && x0 + 1 <= hi + 1) fold_speed<S, T>(Fb, a.P, smax);
+      if (x0 - 2 >= lo && x0 - 2 < hi) {
+        T* dst = orow + (x0 - 2);
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          dst[k * a.sstride] = oA[k];
+          fin = min(fin, finite_key(oA[k]));
+        }
+      }
+      if (x0 - 1 >= lo && x0 - 1 < hi) {
+        T* dst = orow + (x0 - 1);
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          dst[k * a.sstride] = oB[k];
+          fin = min(fin, finite_key(oB[k]));
+        }
+      }
+      __syncwarp();
+      if (lane == 31) {
+        T* slot = carry[wib];
+        int i = 0;
+        S::for_cell_regs(c1, [&](T& r) { slot[i++] = r; });
+        S::for_regs(Fa, [&](T& r) { slot[i++] = r; });
+        S::for_regs(Fb, [&](T& r) { slot[i++] = r; });
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          slot[KC + 2 * KF + k] = Ga[k];
+          slot[KC + 2 * KF + M + k] = q0[k];
+          slot[KC + 2 * KF + 2 * M + k] = q1[k];
+        }
+      }
+      __syncwarp();
+      cur ^= 1;
+    }
+  }
+  finish_block<T>(smax, fin, a);
+}
+
+// ---------------------------------------------------------------------------
 // Per-interface solve for the Riemann-plugin parity unit (riemann.py:205-223).
 template <typename T, class S>
 __global__ void solve_pairs(const T* ql, const T* qr, T* W, T* s, int64_t n, Params<T> P) {
@@ -1480,9 +1685,22 @@ inline cudaError_t launch_contig_shfl(const GenericArgs& g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <typename T, class S, int LIM, bool LIT>
+inline cudaError_t launch_pair(const GenericArgs& g, cudaStream_t st) {
+  if (g.occ_out)
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(g.occ_out, sweep_pair<T, S, LIM, LIT>,
+                                                         128, 0);
+  SweepArgs<T> a = to_args<T>(g);
+  const int64_t warps = (int64_t)g.n1 * g.n2 * g.nseg;
+  const int64_t blocks = (warps + 3) / 4;
+  sweep_pair<T, S, LIM, LIT><<<(unsigned)blocks, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, class S, int LIM, bool LIT, bool CONTIG>
 inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
   if (CONTIG && g.contig == 1) return launch_contig_shfl<T, S, LIM, LIT>(g, st);
+  if (CONTIG && g.contig == 3) return launch_pair<T, S, LIM, LIT>(g, st);
   constexpr int kSmem = (CONTIG && !CLB_X_LEGACY) ? XGeom<T, S>::SMEM
                                                    : StageGeom<T, S, CONTIG>::SMEM;
   // the dynamic shared-memory opt-in is per device: one bit per device

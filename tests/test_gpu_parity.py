@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import paper_1805_08846_b200 as P
-from paper_1805_08846_b200._native import XVAR_AUTO, XVAR_MARCH, XVAR_TMA, DeviceGrid
+from paper_1805_08846_b200._native import XVAR_AUTO, XVAR_MARCH, XVAR_PAIR, XVAR_TMA, DeviceGrid
 from oracle import oracle as O
 
 import cases
@@ -27,8 +27,8 @@ def _grid_from_padded(qin, c):
     return g
 
 
-@pytest.mark.parametrize("variant", [XVAR_AUTO, XVAR_MARCH, XVAR_TMA],
-                         ids=["auto", "x-march", "x-tma"])
+@pytest.mark.parametrize("variant", [XVAR_AUTO, XVAR_MARCH, XVAR_TMA, XVAR_PAIR],
+                         ids=["auto", "x-march", "x-tma", "x-pair"])
 def test_golden_sweeps_bitwise(golden_sweeps, variant):
     meta, arrays = golden_sweeps
     bad = []
@@ -149,7 +149,8 @@ def _recipe(problem, cells, profile, options, dtype, bc, limiter, steps):
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 @pytest.mark.parametrize("bc", ["outflow", "reflective", "periodic"])
 @pytest.mark.parametrize("limiter", ["mc", "superbee", "minmod", "vanleer", "none"])
-@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA], ids=["x-march", "x-tma"])
+@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA, XVAR_PAIR],
+                         ids=["x-march", "x-tma", "x-pair"])
 def test_random_configs_match_oracle(shape, dtype, bc, limiter, variant):
     """Both x-sweep kernels (forced per handle) on every shape / BC / limiter."""
     problem, cells, profile, options = shape
@@ -165,7 +166,8 @@ def test_random_configs_match_oracle(shape, dtype, bc, limiter, variant):
         assert sim.grid.interior().tobytes() == O.interior(osim.grid).tobytes()
 
 
-@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA], ids=["x-march", "x-tma"])
+@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA, XVAR_PAIR],
+                         ids=["x-march", "x-tma", "x-pair"])
 @pytest.mark.parametrize("seg", [(1, 1), (7, 5), (33, 40), (64, 3), (1000, 1000)])
 def test_segmentation_is_bitwise_invisible(seg, variant):
     r = _recipe("shallow_water2d", (150, 130), "radial_dam_break", {}, "float64", "reflective",
@@ -351,7 +353,8 @@ def test_fast_division_and_sqrt_are_bitwise_ieee(rng):
     assert min(dfall, sfall, fdfall, fsfall, lfall, rfall) > 0
 
 
-@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA], ids=["x-march", "x-tma"])
+@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA, XVAR_PAIR],
+                         ids=["x-march", "x-tma", "x-pair"])
 @pytest.mark.parametrize("limiter", ["mc", "vanleer", "superbee"])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_slow_path_inputs_match_oracle(rng, limiter, dtype, variant):

@@ -23,7 +23,7 @@ import numpy as np
 import pytest
 
 import paper_1805_08846_b200 as P
-from paper_1805_08846_b200._native import XVAR_MARCH, XVAR_TMA
+from paper_1805_08846_b200._native import XVAR_MARCH, XVAR_PAIR, XVAR_TMA
 from oracle import oracle as O
 
 import cases
@@ -85,14 +85,14 @@ def test_c2_sw1024_100_steps_with_revert():
     assert sum(1 for a in att if not a.accepted) >= 1
 
 
-@pytest.mark.parametrize("variant", [None, XVAR_MARCH],
-                         ids=["auto-tma", "warp-march"])
+@pytest.mark.parametrize("variant", [None, XVAR_MARCH, XVAR_PAIR],
+                         ids=["auto-tma", "warp-march", "pair-march"])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_sw2048_tma_x_sweep_with_revert(dtype, variant):
     r = _recipe("sw2048", "shallow_water2d", (2048, 2048), "radial_dam_break", dtype,
                 "reflective", "mc", 3, speed=("scale", 0.5))
     att, used = _run_both(r, variant)
-    assert used == (XVAR_TMA if variant is None else XVAR_MARCH)
+    assert used == (XVAR_TMA if variant is None else variant)
     assert not att[0].accepted and att[1].accepted
 
 
@@ -129,3 +129,10 @@ def test_c5_acoustics_512cube_periodic(dtype):
     r = _recipe("c5", "acoustics3d", (512, 512, 512), "gaussian_pressure", dtype, "periodic",
                 "mc", 2, options={"width": 0.1})
     _run_both(r)
+
+
+def test_c5_acoustics_pair_march_x():
+    r = _recipe("c5", "acoustics3d", (512, 512, 256), "gaussian_pressure", "float64",
+                "periodic", "superbee", 2, options={"width": 0.1})
+    _, used = _run_both(r, XVAR_PAIR)
+    assert used == XVAR_PAIR
