@@ -737,7 +737,8 @@ int clb_create(const clb_desc* desc, clb_handle* out) {
   {
     // process-wide default of clb_set_x_variant: CLB_CONTIG=tma|shfl
     const char* e = getenv("CLB_CONTIG");
-    h->x_variant = e ? (e[0] == 't' ? CLB_XVAR_TMA : CLB_XVAR_MARCH) : CLB_XVAR_AUTO;
+    h->x_variant = e ? (e[0] == 't' ? CLB_XVAR_TMA : e[0] == 'p' ? CLB_XVAR_PAIR : CLB_XVAR_MARCH)
+                     : CLB_XVAR_AUTO;
   }
   for (int ax = 0; ax < d.ndim; ++ax) h->cells[ax] = d.cells[ax];
   const int64_t align = 128 / d.itemsize;
