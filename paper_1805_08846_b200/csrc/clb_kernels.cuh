@@ -1457,6 +1457,24 @@ __device__ __forceinline__ void pair_chunk(const SweepArgs<T>& a, T dtdx, int li
   update<S, LIT, T>(pq1, Fpb, Fa, Ga, Gm, a.P, dtdx, oB);    // cell x0-1
 }
 
+// every wave component of the fan is +-0 and every register finite
+template <class S, class Fan> __device__ __forceinline__ bool pair_zero_fan(Fan f) {
+  uint32_t key = 0xffffffffu;
+  bool zero = true;
+  S::for_regs(f, [&](auto& r) { key = min(key, finite_key(r)); });
+#pragma unroll
+  for (int p = 0; p < S::NW; ++p) {
+#pragma unroll
+    for (int k = 0; k < S::M; ++k) {
+      if (S::nz(p, k)) {
+        const auto w = S::wave(f, p, k);
+        zero = zero && (w == decltype(w)(0));
+      }
+    }
+  }
+  return zero && key != 0u;
+}
+
 #ifndef CLB_PAIR_MINB
 #define CLB_PAIR_MINB 2
 #endif
@@ -1518,6 +1536,7 @@ __global__ void __launch_bounds__(128, CLB_PAIR_MINB) sweep_pair(const SweepArgs
     const int b0 = lo - 4;
     issue(b0, 0);
     int cur = 0;
+    bool uni_pair = false;  // the carry holds a uniform state (warp-uniform)
     for (int b = b0; b - 2 < hi; b += 64) {
       const bool first = b == b0;
       if (b + 64 - 2 < hi) issue(b + 64, cur ^ 1);
@@ -1539,6 +1558,56 @@ __global__ void __launch_bounds__(128, CLB_PAIR_MINB) sweep_pair(const SweepArgs
           pq0[k] = carry[wib][KC + 2 * KF + M + k];
           pq1[k] = carry[wib][KC + 2 * KF + 2 * M + k];
         }
+      }
+      // Uniform-state skip (exact; see March): when every cell of the chunk
+      // equals the carried cells b-2, b-1 and the carried fans F(b-2), F(b-1)
+      // are finite with only +-0 waves, every fan of the chunk is that same
+      // self-fan, every correction +0, and every output its input: the chunk
+      // only streams.  The carry becomes uniform (F(b+62) = F(b+63) = the
+      // self-fan, G = +0), so following uniform chunks check the cells alone.
+      if constexpr (!LIT && S::kUniformSkip) {
+        if (!first) {
+          const T* cs = carry[wib];
+          T u[M];
+#pragma unroll
+          for (int k = 0; k < M; ++k) u[k] = cs[KC + 2 * KF + 2 * M + k];  // cell b-1
+          bool eq = same_bits<T, M>(q0, u) && same_bits<T, M>(q1, u);
+          if (!uni_pair) {
+            T u0[M];
+#pragma unroll
+            for (int k = 0; k < M; ++k) u0[k] = cs[KC + 2 * KF + M + k];     // cell b-2
+            Fan ca, cb;
+            int i = KC;
+            S::for_regs(ca, [&](T& r) { r = cs[i++]; });
+            S::for_regs(cb, [&](T& r) { r = cs[i++]; });
+            eq = eq && same_bits<T, M>(u0, u) && pair_zero_fan<S>(ca) && pair_zero_fan<S>(cb);
+          }
+          if (__all_sync(FULL, eq)) {
+            if (!uni_pair) {
+              __syncwarp();
+              if (lane == 31) {
+                T* slot = carry[wib];
+                for (int i = 0; i < KF; ++i) slot[KC + i] = slot[KC + KF + i];  // Fa := Fb
+                for (int k = 0; k < M; ++k) slot[KC + 2 * KF + k] = T(0);       // G := +0
+              }
+              __syncwarp();
+              uni_pair = true;
+            }
+            // outputs = inputs (finite: a finite self-fan needs a finite state)
+            if (x0 - 2 >= lo && x0 - 2 < hi) {
+#pragma unroll
+              for (int k = 0; k < M; ++k) orow[(x0 - 2) + k * a.sstride] = u[k];
+            }
+            if (x0 - 1 >= lo && x0 - 1 < hi) {
+#pragma unroll
+              for (int k = 0; k < M; ++k) orow[(x0 - 1) + k * a.sstride] = u[k];
+            }
+            __syncwarp();
+            cur ^= 1;
+            continue;
+          }
+        }
+        uni_pair = false;
       }
       Fan Fa, Fb;
       Cell c1;
