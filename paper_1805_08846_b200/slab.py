@@ -204,7 +204,8 @@ class Slab:
         if self.layout.world == 1 or self.dist is None:
             return values
         import torch
-        dev = "cuda" if self.transport == "nccl" else "cpu"
+        # host transport: gloo (CPU tensors); nccl/device: an NCCL process group
+        dev = "cpu" if self.transport == "host" else "cuda"
         t = torch.tensor(values, dtype=torch.float64, device=dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return t.cpu().numpy()
@@ -213,7 +214,8 @@ class Slab:
         if self.layout.world == 1 or self.dist is None:
             return value
         import torch
-        dev = "cuda" if self.transport == "nccl" else "cpu"
+        # host transport: gloo (CPU tensors); nccl/device: an NCCL process group
+        dev = "cpu" if self.transport == "host" else "cuda"
         t = torch.tensor([value], dtype=torch.int64, device=dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
         return int(t.item())
