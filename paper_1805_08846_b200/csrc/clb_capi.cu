@@ -192,7 +192,7 @@ bool make_tensor_map(clb_ctx* h, int buf, bool store, void* out) {
   // (clb_kernels.cuh XGeom); CLB_X_LEGACY: 48-byte rows, no swizzle
   const bool legacy = CLB_X_LEGACY != 0;
   const int row = legacy ? 48 : clb::x_row_bytes(h->M);
-  cuuint32_t box[4] = {(cuuint32_t)(row / isz), 128u, 1u, 1u};
+  cuuint32_t box[4] = {(cuuint32_t)(row / isz), (cuuint32_t)(legacy ? 128 : clb::kXRows), 1u, 1u};
   cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
   CUresult r = enc((CUtensorMap*)out,
                    isz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
@@ -269,7 +269,8 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
     g.tz0 = h->ndim == 3 ? 2 : 0;
     // warp-marching: one warp per (row, segment), 4 warps per CTA;
     // TMA: 128 rows of one z-plane per CTA
-    pen_ctas = g.contig != 2 ? (ny * nz + 3) / 4 : ((ny + 127) / 128) * nz;
+    pen_ctas = g.contig != 2 ? (ny * nz + 3) / 4
+                             : ((ny + clb::kXRows - 1) / clb::kXRows) * nz;
   } else {
     g.contig = 0;
     g.n1 = (int)nx;

@@ -46,6 +46,9 @@ constexpr int kConsumers = 128;        // pencils per CTA
 #ifndef CLB_X_LEGACY
 #define CLB_X_LEGACY 0
 #endif
+#ifndef CLB_X_ROWS
+#define CLB_X_ROWS 128  // rows per CTA of the TMA x sweep (64 or 128)
+#endif
 // CLB_INLINE_PRODUCER: consumer thread 0 issues the stage copies (no
 // producer warp), so a CTA is 4 warps
 constexpr bool kInlineProducer = CLB_INLINE_PRODUCER != 0;
@@ -61,8 +64,9 @@ constexpr bool kInlineX = CLB_X_INLINE != 0;
 template <bool CONTIG> constexpr bool inline_producer() {
   return (CONTIG && !CLB_X_LEGACY) ? kInlineX : kInlineProducer;
 }
+constexpr int kXRows = CLB_X_ROWS;
 template <bool CONTIG> constexpr int threads_of() {
-  return kConsumers + (inline_producer<CONTIG>() ? 0 : 32);
+  return ((CONTIG && !CLB_X_LEGACY) ? kXRows : kConsumers) + (inline_producer<CONTIG>() ? 0 : 32);
 }
 constexpr int kRowStrideContig = 48;   // bytes per row per state in a contig stage
 
@@ -853,8 +857,9 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 #define CLB_X_NSTAGE 0   // 0: from CLB_X_BUDGET
 #endif
 #ifndef CLB_X_ROW
-#define CLB_X_ROW 64    // box row bytes of the x stages for m <= 3 states (32 or 64)
+#define CLB_X_ROW 64    // box row bytes of the x stages for m <= 3 states (32, 64, 128)
 #endif
+
 #ifndef CLB_X_ROW4
 #define CLB_X_ROW4 32   // box row bytes of the x stages for m >= 4 states (32 or 64)
 #endif
@@ -864,9 +869,10 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 // box row bytes of the x stages (host side: clb_capi.cu make_tensor_map)
 __host__ __device__ constexpr int x_row_bytes(int m) { return m >= 4 ? CLB_X_ROW4 : CLB_X_ROW; }
 template <typename T, class S> struct XGeom {
+  static constexpr int ROWS = kXRows;                   // rows (consumer threads) per CTA
   static constexpr int ROW = x_row_bytes(S::M);         // bytes per row per state
   static constexpr int NC = ROW / (int)sizeof(T);
-  static constexpr int SBYTES = kConsumers * ROW;       // one state of a stage
+  static constexpr int SBYTES = ROWS * ROW;             // one state of a stage
   static constexpr int BYTES = S::M * SBYTES;
   // as many stages as the ring budget holds (in-place outputs need >= 3)
   // the resident CTAs' share of the 228 KB (less static + reserved memory)
@@ -896,8 +902,8 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
   const int nr = len + NC + 2;                 // positions: cells lo-NC .. hi+1
   const int nst = (nr + NC - 1) / NC;
   const int nout = (len + NC - 1) / NC;        // output stages 1 .. nout
-  const int64_t pb = (int64_t)blockIdx.x * kConsumers;
-  const int nvalid = (int)(a.n1 - pb < (int64_t)kConsumers ? a.n1 - pb : (int64_t)kConsumers);
+  const int64_t pb = (int64_t)blockIdx.x * G::ROWS;
+  const int nvalid = (int)(a.n1 - pb < (int64_t)G::ROWS ? a.n1 - pb : (int64_t)G::ROWS);
   const int cy = a.ty0 + (int)pb, cz = a.tz0 + (int)blockIdx.z;
   auto slot = [&](int k) { return (k0 + k) % NSTAGE; };
   auto stage_ptr = [&](int k) { return ring + slot(k) * G::BYTES; };
@@ -912,7 +918,7 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
     for (int q = 0; q < M; ++q)
       tma_load_4d(ring + s * G::BYTES + q * G::SBYTES, map_ld, cx, cy, cz, q, &full[s]);
   };
-  if (!kInlineX && warp == kConsumers / 32) {
+  if (!kInlineX && warp == G::ROWS / 32) {
     if (lane == 0)
       for (int k = 0; k < nst; ++k) produce(k);
     return;
@@ -992,7 +998,7 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
   // output cell e (position NC + e) in place; flush a completed tile
   auto flush = [&](int k) {                     // stage k >= 1 holds tile k-1
     fence_proxy_async_smem();
-    named_barrier_sync(1, kConsumers);
+    named_barrier_sync(1, G::ROWS);
     if (t == 0) {
       const unsigned char* st = stage_ptr(k);
       const int cx = a.tx0 + lo + (k - 1) * NC;
@@ -1097,7 +1103,7 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
   }
   // every slot of the pass goes back once; the stores have completed before
   // the next pass (or the kernel) ends
-  named_barrier_sync(1, kConsumers);
+  named_barrier_sync(1, G::ROWS);
   if (t == 0) {
     bulk_wait<0>();
     release_upto(nst);
@@ -1789,7 +1795,8 @@ inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
                                                                       kSmem);
   SweepArgs<T> a = to_args<T>(g);
   static const TmaMaps none{};
-  dim3 grid((unsigned)((g.n1 + kConsumers - 1) / kConsumers), (unsigned)(g.seg_end - g.seg_begin),
+  constexpr int rows = (CONTIG && !CLB_X_LEGACY) ? kXRows : kConsumers;
+  dim3 grid((unsigned)((g.n1 + rows - 1) / rows), (unsigned)(g.seg_end - g.seg_begin),
             (unsigned)g.n2);
   fn<<<grid, threads_of<CONTIG>(), kSmem, st>>>(a, CONTIG ? *g.maps : none);
   return cudaGetLastError();
