@@ -590,43 +590,14 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
         tma_load_4d(st + q * kConsumers * kRowStrideContig, map_ld, cx, cy, cz, q, &full[s]);
     }
   };
-  // The strided stages are issued by a whole warp: lane 0 arms the barrier,
-  // then one bulk copy per lane (NC rows x M states), so the producer's
-  // issue time is one copy, not NC*M (it matters when the producer is
-  // consumer warp 0 and the consumers skip uniform groups quickly).
-  auto produce_w = [&](int k) {
-    if (CONTIG) {
-      if (lane == 0) produce(k);
-      __syncwarp();
-      return;
-    }
-    constexpr int isz = (int)sizeof(T);
-    const int kk = k0 + k;
-    const int s = kk % NSTAGE;
-    if (kk >= NSTAGE) mbar_wait_sleep(&empty[s], ((kk / NSTAGE) - 1) & 1);
-    unsigned char* st = smem + s * G::BYTES;
-    const uint32_t colbytes = (uint32_t)(((nvalid * isz) + 15) & ~15);
-    const T* base = L.qin + pb + (int64_t)blockIdx.z * a.t2stride;
-    const int r0 = k * NC, r1 = min(ncell, r0 + NC);
-    const int rs = max(r0, A);
-    const int nrow = r1 > rs ? r1 - rs : 0;
-    if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(nrow * M) * colbytes);
-    __syncwarp();
-    for (int j = lane; j < nrow * M; j += 32) {
-      const int r = rs + j / M, q = j - (j / M) * M;
-      bool neg;
-      const int js = remap(lo - 2 - A + r, a.n, a.bc_lo, a.bc_hi, neg);
-      bulk_g2s(st + ((q * NC + (r - r0)) * kConsumers) * isz,
-               base + (int64_t)js * a.astride + q * a.sstride, colbytes, &full[s]);
-    }
-  };
   if (!kInlineProducer && warp == kConsumers / 32) {
-    for (int k = 0; k < nst; ++k) produce_w(k);
+    if (lane == 0)
+      for (int k = 0; k < nst; ++k) produce(k);
     return;
   }
   int issued = 0;   // inline producer: stages of this pass issued so far
-  if (kInlineProducer && warp == 0)
-    for (; issued < min(nst, NSTAGE); ++issued) produce_w(issued);
+  if (kInlineProducer && tid == 0)
+    for (; issued < min(nst, NSTAGE); ++issued) produce(issued);
   // ------------------------------ consumers ------------------------------
   const int t = tid;
   const bool active = t < nvalid;
@@ -785,15 +756,13 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
     // inline producer: issue every stage whose slot is already free (a
     // non-blocking probe of its empty barrier), and block only for stage k
     // itself -- thread 0 never waits for the other warps just to prefetch
-    if (kInlineProducer && warp == 0) {
+    if (kInlineProducer && t == 0) {
       while (issued < nst && issued < k + NSTAGE) {
         const int kq = k0 + issued;
-        // lane 0's probe decides for the warp (the warp issues together)
-        const bool free_slot = __shfl_sync(
-            FULL, (int)(issued <= k || kq < NSTAGE ||
-                        mbar_test_wait(&empty[kq % NSTAGE], ((kq / NSTAGE) - 1) & 1)), 0);
-        if (!free_slot) break;
-        produce_w(issued++);
+        if (issued > k && kq >= NSTAGE &&
+            !mbar_test_wait(&empty[kq % NSTAGE], ((kq / NSTAGE) - 1) & 1))
+          break;
+        produce(issued++);
       }
     }
     mbar_wait(&full[s], (kk / NSTAGE) & 1);
