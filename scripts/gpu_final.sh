@@ -20,4 +20,10 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"swe
   -o $O/prof_hump python bench.py --workload sw8192hump --steps 2 --warmup 3 --no-cpu > $O/ncu_hump.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel" -s 9 -c 3 \
   -o $O/prof_c5 python bench.py --workload c5 --steps 2 --warmup 3 --no-cpu > $O/ncu_c5.log 2>&1
+# summaries on the box; only the C4 report comes back (gpurun_out <= 64 MiB)
+python scripts/ncu_summ.py $O/prof_c4.ncu-rep 268435456 > $O/ncu_c4.txt 2>&1
+python scripts/ncu_summ.py $O/prof_hump.ncu-rep 67108864 > $O/ncu_hump.txt 2>&1
+python scripts/ncu_summ.py $O/prof_c5.ncu-rep 134217728 > $O/ncu_c5.txt 2>&1
+rm -f $O/prof_hump.ncu-rep $O/prof_c5.ncu-rep
+du -sh $O > $O/size.txt
 echo done > $O/DONE
