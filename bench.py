@@ -400,8 +400,11 @@ def run_gpu(args, rank, world, scaling):
     achieved = bytes_per_launch / (mean_ms / 1e3) / 1e9
     peak, peak_kind = measured_peaks()
     xvar = dev.x_variant() if hasattr(dev, "x_variant") else None
-    kname = (("x-sweep (contiguous axis, " + ("TMA tensor-map transpose" if xvar == 2
-                                               else "warp-march") + ")") if dom == 0
+    xname = {2: "TMA tensor-map transpose", 3: "pair warp-march",
+             4: "TMA tensor-map transpose, 64 rows x 128 B",
+             5: "TMA tensor-map transpose, geometry pair selected per attempt"}.get(xvar,
+                                                                                   "warp-march")
+    kname = (("x-sweep (contiguous axis, " + xname + ")") if dom == 0
              else f"axis-{dom} sweep (strided, bulk-copy ring)")
     traffic = ncu_traffic(args.workload, f"axis{dom}")
     sim.close()

@@ -105,13 +105,24 @@ int clb_set_segments(clb_handle h, int axis, int seg_len);
  *   CLB_XVAR_AUTO  (0) by solver and grid size (the measured best),
  *   CLB_XVAR_MARCH (1) warp-marching kernel (one lane per cell, shuffles),
  *   CLB_XVAR_TMA   (2) TMA tensor-map transpose kernel (one thread per row),
- *   CLB_XVAR_PAIR  (3) pair warp-march (two cells per lane, 64-cell chunks).
+ *   CLB_XVAR_PAIR  (3) pair warp-march (two cells per lane, 64-cell chunks),
+ *   CLB_XVAR_TMA_STREAM (4) TMA transpose with the streaming geometry (64
+ *                       rows of 128 bytes; fp64 shallow water only),
+ *   CLB_XVAR_TMA_ADAPT  (5) both TMA geometries launched on every x sweep,
+ *                       the one the previous strided sweep's share of
+ *                       computed (not skipped) cell groups selects does
+ *                       the work (fp64 shallow water only; AUTO's choice
+ *                       for large grids).
  * Results are bitwise independent of the variant; exposed so every variant
  * can be held to the oracle at any size (tests) and for tuning.  The
- * process-wide default is CLB_CONTIG=tma|shfl (read once), else AUTO. */
-enum { CLB_XVAR_AUTO = 0, CLB_XVAR_MARCH = 1, CLB_XVAR_TMA = 2, CLB_XVAR_PAIR = 3 };
+ * process-wide default is CLB_CONTIG=tma|shfl|pair|stream|adapt (read
+ * once), else AUTO. */
+enum {
+  CLB_XVAR_AUTO = 0, CLB_XVAR_MARCH = 1, CLB_XVAR_TMA = 2, CLB_XVAR_PAIR = 3,
+  CLB_XVAR_TMA_STREAM = 4, CLB_XVAR_TMA_ADAPT = 5
+};
 int clb_set_x_variant(clb_handle h, int variant);
-/* The variant the next x sweep of this handle launches (1, 2 or 3). */
+/* The variant the next x sweep of this handle launches (1 .. 5). */
 int clb_x_variant(clb_handle h, int32_t *variant);
 
 /* Interior transfer, frame-payload order: state-major, then z, y, x (x

@@ -41,7 +41,7 @@ EXPORTS = (
 )
 
 #: x-sweep kernel variants (clb_set_x_variant)
-XVAR_AUTO, XVAR_MARCH, XVAR_TMA, XVAR_PAIR = 0, 1, 2, 3
+XVAR_AUTO, XVAR_MARCH, XVAR_TMA, XVAR_PAIR, XVAR_TMA_STREAM, XVAR_TMA_ADAPT = 0, 1, 2, 3, 4, 5
 
 #: clb_run_batch statuses (include/clawb200.h)
 BATCH_STOP, BATCH_MAXSTEPS, BATCH_LOGFULL, BATCH_BLOWUP, BATCH_UNSTABLE, BATCH_DTERR = range(6)
@@ -259,11 +259,12 @@ class DeviceGrid:
         _check(lib().clb_set_segments(self.handle, axis, seg_len), self.handle)
 
     def set_x_variant(self, variant: int):
-        """x-sweep kernel: XVAR_AUTO, XVAR_MARCH (warp-march), XVAR_TMA or XVAR_PAIR."""
+        """x-sweep kernel: XVAR_AUTO, XVAR_MARCH (warp-march), XVAR_TMA, XVAR_PAIR,
+        XVAR_TMA_STREAM or XVAR_TMA_ADAPT (the last two: fp64 2-D shallow water)."""
         _check(lib().clb_set_x_variant(self.handle, int(variant)), self.handle)
 
     def x_variant(self) -> int:
-        """The kernel variant the next x sweep launches (XVAR_MARCH / XVAR_TMA / XVAR_PAIR)."""
+        """The kernel variant the next x sweep launches (XVAR_MARCH .. XVAR_TMA_ADAPT)."""
         v = _i32(0)
         _check(lib().clb_x_variant(self.handle, ctypes.byref(v)), self.handle)
         return int(v.value)

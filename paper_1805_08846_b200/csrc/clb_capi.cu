@@ -58,8 +58,15 @@ struct clb_ctx {
   int num_sms = 148;
   int seg_override[3] = {0, 0, 0};
   int x_variant = 0;        // CLB_XVAR_*: 0 = automatic
-  int resident[3][4] = {};  // [axis][contig mode]: CTAs per SM
+  int resident[3][5] = {};  // [axis][contig mode, 4: streaming x]: CTAs per SM
   clb::TmaMaps maps;        // per buffer: load map, store map
+  clb::TmaMaps maps_xs;     // the same for the streaming x geometry (has_xs)
+  bool have_maps_xs = false;
+  // x geometry pair (CLB_XVAR_TMA_ADAPT): computed cell groups of the strided
+  // sweeps since the last x sweep, and the count below which the streaming
+  // twin works
+  unsigned long long* d_act = nullptr;
+  unsigned long long xs_thresh = 0;
   // device-resident controller (clb_run_batch)
   clb::DevCtl* d_ctl = nullptr;
   clb::DevCtl* h_ctl = nullptr;
@@ -170,7 +177,7 @@ CUtensorMapL2promotion tma_promotion() {
 // 4-D view (x, y, z, state) of one buffer for the contiguous-axis sweep: box =
 // 48 bytes of x by 128 rows.  `store` limits the extent to the interior so
 // tiles that overhang the grid are clipped by the TMA unit.
-bool make_tensor_map(clb_ctx* h, int buf, bool store, void* out) {
+bool make_tensor_map(clb_ctx* h, int buf, bool store, void* out, int xs = 0) {
   auto enc = tensor_map_encoder();
   if (!enc) return false;
   const int isz = h->itemsize;
@@ -191,8 +198,9 @@ bool make_tensor_map(clb_ctx* h, int buf, bool store, void* out) {
   // x stages: 64-byte rows (whole sectors) with the 64-byte swizzle
   // (clb_kernels.cuh XGeom); CLB_X_LEGACY: 48-byte rows, no swizzle
   const bool legacy = CLB_X_LEGACY != 0;
-  const int row = legacy ? 48 : clb::x_row_bytes(h->M);
-  cuuint32_t box[4] = {(cuuint32_t)(row / isz), (cuuint32_t)(legacy ? 128 : clb::kXRows), 1u, 1u};
+  const int row = legacy ? 48 : clb::x_row_bytes(h->M, xs);
+  const int rows = legacy ? 128 : (xs ? clb::x_rows<1>() : clb::x_rows<0>());
+  cuuint32_t box[4] = {(cuuint32_t)(row / isz), (cuuint32_t)rows, 1u, 1u};
   cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
   CUresult r = enc((CUtensorMap*)out,
                    isz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
@@ -210,7 +218,7 @@ cudaError_t dispatch_family(clb_ctx* h, int axis, bool literal, const clb::Gener
 // Resident CTAs per SM of the (non-literal) sweep kernel the geometry selects
 // (cudaOccupancyMaxActiveBlocksPerMultiprocessor, cached per axis and mode).
 int resident_ctas(clb_ctx* h, int axis, const clb::GenericArgs& g0) {
-  int& r = h->resident[axis][g0.contig];
+  int& r = h->resident[axis][g0.xs ? 4 : g0.contig];
   if (r == 0) {
     clb::GenericArgs g = g0;
     int occ = 0;
@@ -221,8 +229,35 @@ int resident_ctas(clb_ctx* h, int axis, const clb::GenericArgs& g0) {
   return r;
 }
 
-// Geometry of one sweep: which kernel, extents and strides.
-clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
+// The x-sweep variant a handle runs (CLB_XVAR_*, never AUTO).
+// x-sweep kernel: the TMA tensor-map variant wins when the march is
+// compute-heavy (fp64 shallow water, profiles/r1_notes.md); the warp-shuffle
+// variant wins elsewhere.  Small grids (C2, 1024^2) have too few 128-row
+// blocks for the TMA variant and run faster warp-marching (56 vs 69 us).
+// 3-D acoustics (m = 4) also streams x faster through the TMA transpose
+// with 32-byte rows on large grids (C5 fp64 x 2.20 vs 2.39 ms, r2j).  fp64
+// shallow water pairs the two TMA geometries (CLB_XVAR_TMA_ADAPT).
+// clb_set_x_variant (per handle) overrides.
+int x_mode(const clb_ctx* h) {
+  int v = h->x_variant;
+  if (v == CLB_XVAR_AUTO) {
+    const int64_t ncells = h->cells[0] * h->cells[1] * h->cells[2];
+    const bool big = ncells >= ((int64_t)1 << 22);
+    v = (big && (h->d.solver_id == CLB_SOLVER_SHALLOW_WATER ||
+                 (h->d.solver_id == CLB_SOLVER_ACOUSTICS && h->ndim == 3)))
+            ? (h->have_maps_xs ? CLB_XVAR_TMA_ADAPT : CLB_XVAR_TMA)
+            : CLB_XVAR_MARCH;
+  }
+  if (v == CLB_XVAR_TMA && !h->have_maps) v = CLB_XVAR_MARCH;
+  if ((v == CLB_XVAR_TMA_STREAM || v == CLB_XVAR_TMA_ADAPT) && !h->have_maps_xs)
+    v = h->have_maps ? CLB_XVAR_TMA : CLB_XVAR_MARCH;
+  return v;
+}
+
+// Geometry of one sweep: which kernel, extents and strides (xs = 1: the
+// streaming twin of the TMA x sweep; -1: the default geometry whatever the
+// variant, for the literal kernels, which have no streaming twin).
+clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst, int xs = 0) {
   clb::GenericArgs g;
   std::memset(&g, 0, sizeof(g));
   const int64_t isz = h->itemsize;
@@ -246,31 +281,21 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   // neighbour; CLB_MIN_SEG overrides, profiles/r1_notes.md).
   const int64_t target_ctas = (int64_t)h->num_sms * 6;
   int64_t pen_ctas;
-  // x-sweep kernel: the TMA tensor-map variant wins when the march is
-  // compute-heavy (fp64 shallow water, profiles/r1_notes.md); the warp-shuffle
-  // variant wins elsewhere.  Small grids (C2, 1024^2) have too few 128-row
-  // blocks for the TMA variant and run faster warp-marching (56 vs 69 us).
-  // clb_set_x_variant (per handle) overrides.
-  const int64_t ncells = h->cells[0] * h->cells[1] * h->cells[2];
-  // 3-D acoustics (m = 4) also streams x faster through the TMA transpose
-  // with 32-byte rows on large grids (C5 fp64 x 2.20 vs 2.39 ms, r2j)
-  const bool big = ncells >= ((int64_t)1 << 22);
-  const int contig_mode = h->x_variant ? h->x_variant
-                          : (big && (h->d.solver_id == CLB_SOLVER_SHALLOW_WATER ||
-                                     (h->d.solver_id == CLB_SOLVER_ACOUSTICS && h->ndim == 3)))
-                                ? 2 : 1;
+  const int mode = x_mode(h);
   if (axis == 0) {
-    g.contig = contig_mode == 2 ? (h->have_maps ? 2 : 1) : contig_mode;
+    g.contig = mode >= CLB_XVAR_TMA_STREAM ? 2 : mode;
+    g.xs = xs < 0 ? 0 : (xs > 0 || mode == CLB_XVAR_TMA_STREAM) ? 1 : 0;
     g.n = (int)nx; g.n1 = (int)ny; g.n2 = (int)nz;
     g.astride = 1; g.t1stride = h->ystride; g.t2stride = h->zstride;
-    g.maps = &h->maps;
+    g.maps = g.xs ? &h->maps_xs : &h->maps;
     g.tx0 = (int)h->xoff;
     g.ty0 = h->ndim >= 2 ? 2 : 0;
     g.tz0 = h->ndim == 3 ? 2 : 0;
     // warp-marching: one warp per (row, segment), 4 warps per CTA;
     // TMA: 128 rows of one z-plane per CTA
     pen_ctas = g.contig != 2 ? (ny * nz + 3) / 4
-                             : ((ny + clb::kXRows - 1) / clb::kXRows) * nz;
+                             : ((ny + clb::x_rows<0>() - 1) / clb::x_rows<0>()) * nz;
+    if (g.xs) pen_ctas = ((ny + clb::x_rows<1>() - 1) / clb::x_rows<1>()) * nz;
   } else {
     g.contig = 0;
     g.n1 = (int)nx;
@@ -284,7 +309,8 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst) {
   }
   // contig stages are 64 (legacy: 48) bytes of a row: segment starts stay aligned
   const int64_t align =
-      (axis == 0 && g.contig == 2) ? (CLB_X_LEGACY ? 48 : clb::x_row_bytes(h->M)) / h->itemsize : 1;
+      (axis == 0 && g.contig == 2) ? (CLB_X_LEGACY ? 48 : clb::x_row_bytes(h->M, g.xs)) / h->itemsize
+                                   : 1;
   static const int64_t min_seg = [] {
     const char* e = getenv("CLB_MIN_SEG");
     return e ? std::max<int64_t>(4, atoll(e)) : (int64_t)16;
@@ -511,7 +537,17 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
   if (!(dt > 0.0)) return fail(h, CLB_EINVAL, "dt must be positive");
   if (slot < 0 || slot > 3) return fail(h, CLB_EINVAL, "result slot out of range");
   cudaSetDevice(h->d.device);  // handles on several devices in one process
-  clb::GenericArgs g = sweep_geometry(h, axis, src, dst);
+  clb::GenericArgs g = sweep_geometry(h, axis, src, dst, literal ? -1 : 0);
+  // x geometry pair: both twins launch, the count selects the working one
+  const bool paired = x_mode(h) == CLB_XVAR_TMA_ADAPT;
+  if (paired) {
+    if (axis == 0 && !literal) {
+      g.xsel = h->d_act;
+      g.xsel_thresh = h->xs_thresh;
+    } else if (axis > 0) {
+      g.act = h->d_act;
+    }
+  }
   g.ctl = indirect ? h->d_ctl : nullptr;
   g.fuse_ctl = (indirect && fuse) ? 1 : 0;
   g.res = h->d_res;
@@ -536,6 +572,19 @@ int launch_sweep(clb_ctx* h, int axis, double dt, int src, int dst, int slot, bo
   }
   cudaError_t e = dispatch_family(h, axis, literal, g, h->stream);
   if (e != cudaSuccess) return cuda_fail(h, e, "sweep launch");
+  if (paired && axis == 0) {
+    if (!literal) {
+      clb::GenericArgs g1 = sweep_geometry(h, axis, src, dst, 1);
+      g1.ctl = g.ctl; g1.fuse_ctl = g.fuse_ctl; g1.res = g.res; g1.dtdx = g.dtdx;
+      for (int i = 0; i < 4; ++i) g1.params[i] = g.params[i];
+      g1.smax_bits = g.smax_bits; g1.nonfinite = g.nonfinite;
+      g1.xsel = g.xsel; g1.xsel_thresh = g.xsel_thresh;
+      e = dispatch_family(h, axis, literal, g1, h->stream);
+      if (e != cudaSuccess) return cuda_fail(h, e, "sweep launch (streaming x)");
+    }
+    e = cudaMemsetAsync(h->d_act, 0, sizeof(unsigned long long), h->stream);
+    if (e != cudaSuccess) return cuda_fail(h, e, "x selector reset");
+  }
   if (h->timing && !indirect) {
     cudaEventRecord(tl.b, h->stream);
     h->launches.push_back(tl);
@@ -736,10 +785,12 @@ int clb_create(const clb_desc* desc, clb_handle* out) {
   h->M = d.num_states;
   h->itemsize = d.itemsize;
   {
-    // process-wide default of clb_set_x_variant: CLB_CONTIG=tma|shfl
+    // process-wide default of clb_set_x_variant: CLB_CONTIG=tma|shfl|pair|stream|adapt
     const char* e = getenv("CLB_CONTIG");
-    h->x_variant = e ? (e[0] == 't' ? CLB_XVAR_TMA : e[0] == 'p' ? CLB_XVAR_PAIR : CLB_XVAR_MARCH)
-                     : CLB_XVAR_AUTO;
+    const std::string v = e ? e : "";
+    h->x_variant = v == "tma" ? CLB_XVAR_TMA : v == "pair" ? CLB_XVAR_PAIR
+                   : v == "stream" ? CLB_XVAR_TMA_STREAM : v == "adapt" ? CLB_XVAR_TMA_ADAPT
+                   : v == "shfl" || v == "march" ? CLB_XVAR_MARCH : CLB_XVAR_AUTO;
   }
   for (int ax = 0; ax < d.ndim; ++ax) h->cells[ax] = d.cells[ax];
   const int64_t align = 128 / d.itemsize;
@@ -780,6 +831,30 @@ int clb_create(const clb_desc* desc, clb_handle* out) {
   for (int b = 0; b < 3 && h->have_maps; ++b)
     if (!(make_tensor_map(h, b, false, h->maps.ld[b]) && make_tensor_map(h, b, true, h->maps.st[b])))
       h->have_maps = false;
+  // the streaming x twin (built-in fp64 2-D shallow water only)
+  if (h->have_maps && d.solver_id == CLB_SOLVER_SHALLOW_WATER && d.itemsize == 8 && d.ndim == 2 &&
+      !CLB_X_LEGACY) {
+    h->have_maps_xs = true;
+    for (int b = 0; b < 3 && h->have_maps_xs; ++b)
+      if (!(make_tensor_map(h, b, false, h->maps_xs.ld[b], 1) &&
+            make_tensor_map(h, b, true, h->maps_xs.st[b], 1)))
+        h->have_maps_xs = false;
+    if (h->have_maps_xs) {
+      // warp groups of a strided sweep: 32 columns x 3 cells each; the
+      // streaming twin works while fewer than CLB_XS_FRAC of them (default
+      // 0.08) were computed
+      static const double frac = [] {
+        const char* f = getenv("CLB_XS_FRAC");
+        return f ? atof(f) : 0.08;
+      }();
+      const double groups = (double)((h->cells[0] + 31) / 32) * (double)((h->cells[1] + 2) / 3);
+      h->xs_thresh = (unsigned long long)(frac * groups);
+      // before any strided sweep: the default geometry
+      if (cudaMalloc(&h->d_act, sizeof(unsigned long long)) != cudaSuccess ||
+          cudaMemsetAsync(h->d_act, 0xff, sizeof(unsigned long long), h->stream) != cudaSuccess)
+        h->have_maps_xs = false;
+    }
+  }
   e = cudaMalloc(&h->d_res, sizeof(Result));
   if (e == cudaSuccess) e = cudaMallocHost(&h->h_res, sizeof(Result));
   if (e == cudaSuccess) e = cudaMemsetAsync(h->d_res, 0, sizeof(Result), h->stream);
@@ -802,6 +877,7 @@ int clb_destroy(clb_handle h) {
   for (int i = 0; i < 3; ++i)
     if (h->buf[i]) cudaFree(h->buf[i]);
   if (h->d_res) cudaFree(h->d_res);
+  if (h->d_act) cudaFree(h->d_act);
   if (h->h_res) cudaFreeHost(h->h_res);
   if (h->batch_exec) cudaGraphExecDestroy(h->batch_exec);
   if (h->batch_graph) cudaGraphDestroy(h->batch_graph);
@@ -840,10 +916,13 @@ int clb_set_segments(clb_handle h, int axis, int seg_len) {
 
 int clb_set_x_variant(clb_handle h, int variant) {
   if (!h) return fail(nullptr, CLB_EINVAL, "null handle");
-  if (variant < CLB_XVAR_AUTO || variant > CLB_XVAR_PAIR)
+  if (variant < CLB_XVAR_AUTO || variant > CLB_XVAR_TMA_ADAPT)
     return fail(h, CLB_EINVAL, "unknown x-sweep variant");
   if (variant == CLB_XVAR_TMA && !h->have_maps)
     return fail(h, CLB_EUNSUPPORTED, "TMA tensor maps unavailable on this device");
+  if ((variant == CLB_XVAR_TMA_STREAM || variant == CLB_XVAR_TMA_ADAPT) && !h->have_maps_xs)
+    return fail(h, CLB_EUNSUPPORTED,
+                "the streaming x geometry exists for fp64 2-D shallow water only");
   h->x_variant = variant;
   drop_batch_graph(h);
   return CLB_OK;
@@ -851,8 +930,7 @@ int clb_set_x_variant(clb_handle h, int variant) {
 
 int clb_x_variant(clb_handle h, int32_t* variant) {
   if (!h || !variant) return fail(h, CLB_EINVAL, "null argument");
-  const clb::GenericArgs g = sweep_geometry(h, 0, 0, 1);
-  *variant = g.contig;
+  *variant = x_mode(h);
   return CLB_OK;
 }
 

@@ -65,8 +65,24 @@ template <bool CONTIG> constexpr bool inline_producer() {
   return (CONTIG && !CLB_X_LEGACY) ? kInlineX : kInlineProducer;
 }
 constexpr int kXRows = CLB_X_ROWS;
-template <bool CONTIG> constexpr int threads_of() {
-  return ((CONTIG && !CLB_X_LEGACY) ? kXRows : kConsumers) + (inline_producer<CONTIG>() ? 0 : 32);
+// XS = 1: the streaming geometry of the TMA x sweep (fp64 shallow water):
+// 64 rows of 128 bytes per box.  It streams a mostly skipped sweep ~8%
+// faster than the default 128 rows x 64 B but leaves fewer warps for active
+// flow; the host launches both and each reads the previous strided sweep's
+// active-group count to decide which one works (profiles/r2_notes.md r2s).
+#ifndef CLB_XS_ROWS
+#define CLB_XS_ROWS 64
+#endif
+#ifndef CLB_XS_ROW
+#define CLB_XS_ROW 128
+#endif
+#ifndef CLB_XS_MINB
+#define CLB_XS_MINB 5
+#endif
+template <int XS> constexpr int x_rows() { return XS ? CLB_XS_ROWS : kXRows; }
+template <bool CONTIG, int XS = 0> constexpr int threads_of() {
+  return ((CONTIG && !CLB_X_LEGACY) ? x_rows<XS>() : kConsumers) +
+         (inline_producer<CONTIG>() ? 0 : 32);
 }
 constexpr int kRowStrideContig = 48;   // bytes per row per state in a contig stage
 
@@ -122,6 +138,12 @@ template <typename T> struct SweepArgs {
   // controller launch per attempt)
   int fuse_ctl;
   Result* res;
+  // x geometry pair (sweep_kernel): non-null on both x launches of a pair;
+  // the streaming twin works when *xsel < xsel_thresh.  act: strided sweeps
+  // add their computed (not skipped) cell groups, one atomic per warp.
+  const unsigned long long* xsel;
+  unsigned long long xsel_thresh;
+  unsigned long long* act;
 };
 
 // TMA descriptors of the three buffers (load: full padded extent; store:
@@ -287,7 +309,8 @@ __device__ __forceinline__ void finish_block(T smax, uint32_t fin, const SweepAr
 #ifndef CLB_SW_MINB_X_INL
 #define CLB_SW_MINB_X_INL 3
 #endif
-template <typename T, class S, bool CONTIG> constexpr int kMinBlocks() {
+template <typename T, class S, bool CONTIG, int XS = 0> constexpr int kMinBlocks() {
+  if (XS) return CLB_XS_MINB;
   if (CONTIG && !CLB_X_LEGACY && kInlineX)
     return (sizeof(T) == 8 && S::NW >= 3) ? CLB_SW_MINB_X_INL : CLB_X_MINB;
   if (kInlineProducer)
@@ -611,6 +634,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
   mr.cool = 0;
   mr.back = 0;
   mr.dtdx = L.dtdx;
+  unsigned nact = 0;  // computed (not skipped) groups of this warp (a.act)
   const T* pin;
   T* pout;
   if (CONTIG) {
@@ -791,6 +815,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
           }
           mr.uni = false;
         }
+        ++nact;
         T o[M];
         bool v;
         v = r0 < ncell;
@@ -828,6 +853,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
     if (last > flushed) flush(last);
     if (t == 0) bulk_wait<0>();
   }
+  if (!CONTIG && a.act && lane == 0 && nact) atomicAdd(a.act, (unsigned long long)nact);
   smax = mr.smax;
   fin = mr.fin;
   bad = mr.bad && active;
@@ -867,28 +893,34 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 #define CLB_X_BUDGET 0   // stage-ring bytes; 0: the share of the resident CTAs
 #endif
 // box row bytes of the x stages (host side: clb_capi.cu make_tensor_map)
-__host__ __device__ constexpr int x_row_bytes(int m) { return m >= 4 ? CLB_X_ROW4 : CLB_X_ROW; }
-template <typename T, class S> struct XGeom {
-  static constexpr int ROWS = kXRows;                   // rows (consumer threads) per CTA
-  static constexpr int ROW = x_row_bytes(S::M);         // bytes per row per state
+__host__ __device__ constexpr int x_row_bytes(int m, int xs = 0) {
+  return xs ? CLB_XS_ROW : (m >= 4 ? CLB_X_ROW4 : CLB_X_ROW);
+}
+// the x geometries with a streaming twin (XS = 1): fp64 shallow water
+template <typename T, class S> constexpr bool has_xs() {
+  return sizeof(T) == 8 && S::M == 3 && S::NW >= 3 && !CLB_X_LEGACY;
+}
+template <typename T, class S, int XS = 0> struct XGeom {
+  static constexpr int ROWS = x_rows<XS>();             // rows (consumer threads) per CTA
+  static constexpr int ROW = x_row_bytes(S::M, XS);     // bytes per row per state
   static constexpr int NC = ROW / (int)sizeof(T);
   static constexpr int SBYTES = ROWS * ROW;             // one state of a stage
   static constexpr int BYTES = S::M * SBYTES;
   // as many stages as the ring budget holds (in-place outputs need >= 3)
   // the resident CTAs' share of the 228 KB (less static + reserved memory)
   static constexpr int BUDGET =
-      CLB_X_BUDGET > 0 ? CLB_X_BUDGET : (228 * 1024) / kMinBlocks<T, S, true>() - 3 * 1024;
+      CLB_X_BUDGET > 0 ? CLB_X_BUDGET : (228 * 1024) / kMinBlocks<T, S, true, XS>() - 3 * 1024;
   static constexpr int NSTAGE_RAW = CLB_X_NSTAGE > 0 ? CLB_X_NSTAGE : BUDGET / BYTES;
   static constexpr int NSTAGE = NSTAGE_RAW < 3 ? 3 : (NSTAGE_RAW > 8 ? 8 : NSTAGE_RAW);
   static constexpr int SMEM = NSTAGE * BYTES + 2 * NSTAGE * 8 + 1024;  // + 1024-B alignment slack
 };
 
-template <typename T, class S, int LIM, bool LIT, class D>
+template <typename T, class S, int LIM, bool LIT, class D, int XS>
 __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live<T>& L,
                                                const TmaMaps& maps_all, unsigned char* ring,
                                                uint64_t* full, uint64_t* empty, int k0,
                                                T& smax, uint32_t& fin, bool& bad) {
-  using G = XGeom<T, S>;
+  using G = XGeom<T, S, XS>;
   constexpr int NC = G::NC, NSTAGE = G::NSTAGE, M = S::M;
   constexpr int isz = (int)sizeof(T);
   const unsigned char* map_ld = maps_all.ld[L.src];
@@ -1134,20 +1166,26 @@ __device__ __forceinline__ int segment_stages(const SweepArgs<T>& a) {
 // ExactArith: it rewrites every output of the segment (same threads, or the
 // same TMA-issuing thread after bulk_wait), and its (smax, fin) replace pass
 // 1's.  Literal (blow-up) kernels run one ExactArith pass.
-template <typename T, class S, int LIM, bool LIT, bool CONTIG>
-__global__ void __launch_bounds__(threads_of<CONTIG>(), kMinBlocks<T, S, CONTIG>())
+template <typename T, class S, int LIM, bool LIT, bool CONTIG, int XS = 0>
+__global__ void __launch_bounds__(threads_of<CONTIG, XS>(), kMinBlocks<T, S, CONTIG, XS>())
     sweep_kernel(const SweepArgs<T> a, const __grid_constant__ TmaMaps maps) {
+  // x geometry pair: only the twin the previous strided sweep's activity
+  // selects does the work (every CTA reads the same count: it is reset after
+  // both x launches and accumulated by the next strided sweep)
+  if (CONTIG && a.xsel && ((*(volatile const unsigned long long*)a.xsel < a.xsel_thresh) != (XS == 1)))
+    return;
   Live<T> L;
   if (!resolve_live(a, L)) return;
   constexpr bool XNEW = CONTIG && !CLB_X_LEGACY;
   using G = StageGeom<T, S, CONTIG>;
-  constexpr int NSTAGE = XNEW ? XGeom<T, S>::NSTAGE : G::NSTAGE;
+  using XG = XGeom<T, S, XS>;
+  constexpr int NSTAGE = XNEW ? XG::NSTAGE : G::NSTAGE;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // the swizzled x stages need 1024-byte aligned buffers
   unsigned char* smem = XNEW ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u)
                              : smem_raw;
   uint64_t* full = reinterpret_cast<uint64_t*>(
-      smem + (XNEW ? NSTAGE * XGeom<T, S>::BYTES : (NSTAGE + G::NOUT) * G::BYTES));
+      smem + (XNEW ? NSTAGE * XG::BYTES : (NSTAGE + G::NOUT) * G::BYTES));
   uint64_t* empty = full + NSTAGE;
 
   if (threadIdx.x == 0) {
@@ -1166,7 +1204,7 @@ __global__ void __launch_bounds__(threads_of<CONTIG>(), kMinBlocks<T, S, CONTIG>
   auto pass = [&](auto arith, int k0) {
     using D = decltype(arith);
     if constexpr (XNEW)
-      segment_pass_x<T, S, LIM, LIT, D>(a, L, maps, smem, full, empty, k0, smax, fin, bad);
+      segment_pass_x<T, S, LIM, LIT, D, XS>(a, L, maps, smem, full, empty, k0, smax, fin, bad);
     else
       segment_pass<T, S, LIM, LIT, CONTIG, D>(a, L, maps, smem, full, empty, k0, smax, fin, bad);
   };
@@ -1174,7 +1212,7 @@ __global__ void __launch_bounds__(threads_of<CONTIG>(), kMinBlocks<T, S, CONTIG>
     if constexpr (XNEW) {
       const int lo = (blockIdx.y + a.seg_base) * a.seg_len;
       const int len = min(a.n, lo + a.seg_len) - lo;
-      constexpr int NC = XGeom<T, S>::NC;
+      constexpr int NC = XG::NC;
       return (len + NC + 2 + NC - 1) / NC;
     } else {
       return segment_stages<T, S, CONTIG>(a);
@@ -1721,6 +1759,10 @@ struct GenericArgs {
   int* occ_out;            // non-null: report resident CTAs per SM instead of launching
   int fuse_ctl;
   Result* res;
+  int xs;                  // 1: the streaming x geometry (XS = 1 twin)
+  const unsigned long long* xsel;
+  unsigned long long xsel_thresh;
+  unsigned long long* act;
 };
 
 template <typename T>
@@ -1745,6 +1787,9 @@ inline SweepArgs<T> to_args(const GenericArgs& g) {
   for (int i = 0; i < 3; ++i) a.bufs[i] = g.bufs[i];
   a.fuse_ctl = g.fuse_ctl;
   a.res = g.res;
+  a.xsel = g.xsel;
+  a.xsel_thresh = g.xsel_thresh;
+  a.act = g.act;
   return a;
 }
 
@@ -1772,16 +1817,16 @@ inline cudaError_t launch_pair(const GenericArgs& g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <typename T, class S, int LIM, bool LIT, bool CONTIG>
+template <typename T, class S, int LIM, bool LIT, bool CONTIG, int XS = 0>
 inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
   if (CONTIG && g.contig == 1) return launch_contig_shfl<T, S, LIM, LIT>(g, st);
   if (CONTIG && g.contig == 3) return launch_pair<T, S, LIM, LIT>(g, st);
-  constexpr int kSmem = (CONTIG && !CLB_X_LEGACY) ? XGeom<T, S>::SMEM
+  constexpr int kSmem = (CONTIG && !CLB_X_LEGACY) ? XGeom<T, S, XS>::SMEM
                                                    : StageGeom<T, S, CONTIG>::SMEM;
   // the dynamic shared-memory opt-in is per device: one bit per device
   // ordinal, set once (atomically: service threads may launch concurrently)
   static std::atomic<unsigned long long> configured{0ull};
-  auto fn = sweep_kernel<T, S, LIM, LIT, CONTIG>;
+  auto fn = sweep_kernel<T, S, LIM, LIT, CONTIG, XS>;
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
@@ -1791,20 +1836,32 @@ inline cudaError_t launch_kernel(const GenericArgs& g, cudaStream_t st) {
     configured.fetch_or(bit, std::memory_order_release);
   }
   if (g.occ_out) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(g.occ_out, fn,
-                                                                      threads_of<CONTIG>(),
+                                                                      threads_of<CONTIG, XS>(),
                                                                       kSmem);
   SweepArgs<T> a = to_args<T>(g);
   static const TmaMaps none{};
-  constexpr int rows = (CONTIG && !CLB_X_LEGACY) ? kXRows : kConsumers;
+  constexpr int rows = (CONTIG && !CLB_X_LEGACY) ? x_rows<XS>() : kConsumers;
   dim3 grid((unsigned)((g.n1 + rows - 1) / rows), (unsigned)(g.seg_end - g.seg_begin),
             (unsigned)g.n2);
-  fn<<<grid, threads_of<CONTIG>(), kSmem, st>>>(a, CONTIG ? *g.maps : none);
+  fn<<<grid, threads_of<CONTIG, XS>(), kSmem, st>>>(a, CONTIG ? *g.maps : none);
   return cudaGetLastError();
 }
 
 template <typename T, class S, bool CONTIG>
 inline cudaError_t launch_lim(const GenericArgs& g, bool literal, cudaStream_t st) {
   if (literal) return launch_kernel<T, S, -1, true, CONTIG>(g, st);
+  if constexpr (CONTIG && has_xs<T, S>()) {
+    if (g.xs) {
+      switch (g.lim_id) {
+        case 0: return launch_kernel<T, S, 0, false, true, 1>(g, st);
+        case 1: return launch_kernel<T, S, 1, false, true, 1>(g, st);
+        case 2: return launch_kernel<T, S, 2, false, true, 1>(g, st);
+        case 3: return launch_kernel<T, S, 3, false, true, 1>(g, st);
+        default: return launch_kernel<T, S, 4, false, true, 1>(g, st);
+      }
+    }
+  }
+  if (g.xs) return cudaErrorInvalidValue;
   switch (g.lim_id) {
     case 0: return launch_kernel<T, S, 0, false, CONTIG>(g, st);
     case 1: return launch_kernel<T, S, 1, false, CONTIG>(g, st);

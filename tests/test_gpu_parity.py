@@ -10,7 +10,8 @@ import numpy as np
 import pytest
 
 import paper_1805_08846_b200 as P
-from paper_1805_08846_b200._native import XVAR_AUTO, XVAR_MARCH, XVAR_PAIR, XVAR_TMA, DeviceGrid
+from paper_1805_08846_b200._native import (XVAR_AUTO, XVAR_MARCH, XVAR_PAIR, XVAR_TMA,
+                                          XVAR_TMA_ADAPT, XVAR_TMA_STREAM, DeviceGrid)
 from oracle import oracle as O
 
 import cases
@@ -27,9 +28,12 @@ def _grid_from_padded(qin, c):
     return g
 
 
-@pytest.mark.parametrize("variant", [XVAR_AUTO, XVAR_MARCH, XVAR_TMA, XVAR_PAIR],
-                         ids=["auto", "x-march", "x-tma", "x-pair"])
+@pytest.mark.parametrize("variant", [XVAR_AUTO, XVAR_MARCH, XVAR_TMA, XVAR_PAIR, XVAR_TMA_STREAM,
+                                     XVAR_TMA_ADAPT],
+                         ids=["auto", "x-march", "x-tma", "x-pair", "x-stream", "x-adapt"])
 def test_golden_sweeps_bitwise(golden_sweeps, variant):
+    """(The streaming / paired x geometries exist for fp64 shallow water
+    only; the other cases run the automatic choice under those ids.)"""
     meta, arrays = golden_sweeps
     bad = []
     for i, c in enumerate(meta):
@@ -62,6 +66,9 @@ def _sweep_exact(grid, out, c, dt, solver, params, variant=XVAR_AUTO):
                    params=solver.pack_params(params, grid.dtype), bc=[(3, 3)] * nd,
                    normal_velocity=[None] * nd)
     try:
+        if variant in (XVAR_TMA_STREAM, XVAR_TMA_ADAPT) and not (
+                c["solver"] == "shallow_water" and grid.dtype == np.float64):
+            variant = XVAR_AUTO
         g.set_x_variant(variant)
         g.upload_padded(0, grid.data)
         smax, _ = g.sweep(c["axis"], dt, 0, 1)
@@ -166,8 +173,46 @@ def test_random_configs_match_oracle(shape, dtype, bc, limiter, variant):
         assert sim.grid.interior().tobytes() == O.interior(osim.grid).tobytes()
 
 
-@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA, XVAR_PAIR],
-                         ids=["x-march", "x-tma", "x-pair"])
+@pytest.mark.parametrize("shape", SHAPES[:2], ids=lambda s: f"{s[0]}-{'x'.join(map(str, s[1]))}")
+@pytest.mark.parametrize("bc", ["outflow", "reflective", "periodic"])
+@pytest.mark.parametrize("limiter", ["mc", "superbee", "minmod", "vanleer", "none"])
+@pytest.mark.parametrize("variant", [XVAR_TMA_STREAM, XVAR_TMA_ADAPT],
+                         ids=["x-stream", "x-adapt"])
+def test_streaming_x_geometry_matches_oracle(shape, bc, limiter, variant):
+    """fp64 shallow water's second TMA x geometry (64 rows x 128 B), forced
+    and paired with the default one (the previous strided sweep's activity
+    selects the twin that works, attempt by attempt)."""
+    problem, cells, profile, options = shape
+    r = _recipe(problem, cells, profile, options, "float64", bc, limiter, steps=6)
+    osim, _ = cases.oracle_sim(r)
+    oatt = cases.drive(osim, r)
+    sim, _ = cases.product_sim(r)
+    with sim:
+        sim.device_grid.set_x_variant(variant)
+        assert sim.device_grid.x_variant() == variant
+        att = cases.drive(sim, r)
+        assert cases.attempts_hex(att) == cases.attempts_hex(oatt)
+        assert sim.grid.interior().tobytes() == O.interior(osim.grid).tobytes()
+
+
+def test_streaming_x_geometry_is_fp64_shallow_water_only():
+    r = _recipe("acoustics2d", (64, 40), "gaussian_pressure", {"width": 0.15}, "float64",
+                "periodic", "mc", steps=1)
+    sim, _ = cases.product_sim(r)
+    with sim:
+        for v in (XVAR_TMA_STREAM, XVAR_TMA_ADAPT):
+            with pytest.raises(Exception, match="fp64 2-D shallow water"):
+                sim.device_grid.set_x_variant(v)
+    r = _recipe("shallow_water2d", (64, 40), "radial_dam_break", {}, "float32", "periodic", "mc",
+                steps=1)
+    sim, _ = cases.product_sim(r)
+    with sim:
+        with pytest.raises(Exception, match="fp64 2-D shallow water"):
+            sim.device_grid.set_x_variant(XVAR_TMA_STREAM)
+
+
+@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA, XVAR_PAIR, XVAR_TMA_STREAM],
+                         ids=["x-march", "x-tma", "x-pair", "x-stream"])
 @pytest.mark.parametrize("seg", [(1, 1), (7, 5), (33, 40), (64, 3), (1000, 1000)])
 def test_segmentation_is_bitwise_invisible(seg, variant):
     r = _recipe("shallow_water2d", (150, 130), "radial_dam_break", {}, "float64", "reflective",
@@ -353,8 +398,8 @@ def test_fast_division_and_sqrt_are_bitwise_ieee(rng):
     assert min(dfall, sfall, fdfall, fsfall, lfall, rfall) > 0
 
 
-@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA, XVAR_PAIR],
-                         ids=["x-march", "x-tma", "x-pair"])
+@pytest.mark.parametrize("variant", [XVAR_MARCH, XVAR_TMA, XVAR_PAIR, XVAR_TMA_STREAM],
+                         ids=["x-march", "x-tma", "x-pair", "x-stream"])
 @pytest.mark.parametrize("limiter", ["mc", "vanleer", "superbee"])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_slow_path_inputs_match_oracle(rng, limiter, dtype, variant):
@@ -362,6 +407,8 @@ def test_slow_path_inputs_match_oracle(rng, limiter, dtype, variant):
     outside their fast-path domain (subnormal and 1e-300-scale momenta, tiny
     depth jumps, exact zeros): the per-step exact recomputation must keep
     every byte equal to the oracle."""
+    if variant == XVAR_TMA_STREAM and dtype != "float64":
+        pytest.skip("the streaming x geometry is fp64 shallow water only")
     spec = P.GridSpec((67, 45), (0.0, 0.0), (1.0, 1.0), 3)
     g = P.create_grid(spec, dtype)
     g.data[0] = 1.0

@@ -23,7 +23,8 @@ import numpy as np
 import pytest
 
 import paper_1805_08846_b200 as P
-from paper_1805_08846_b200._native import XVAR_MARCH, XVAR_PAIR, XVAR_TMA
+from paper_1805_08846_b200._native import (XVAR_MARCH, XVAR_PAIR, XVAR_TMA, XVAR_TMA_ADAPT,
+                                          XVAR_TMA_STREAM)
 from oracle import oracle as O
 
 import cases
@@ -85,14 +86,17 @@ def test_c2_sw1024_100_steps_with_revert():
     assert sum(1 for a in att if not a.accepted) >= 1
 
 
-@pytest.mark.parametrize("variant", [None, XVAR_MARCH, XVAR_PAIR],
-                         ids=["auto-tma", "warp-march", "pair-march"])
+@pytest.mark.parametrize("variant", [None, XVAR_MARCH, XVAR_PAIR, XVAR_TMA, XVAR_TMA_STREAM],
+                         ids=["auto", "warp-march", "pair-march", "tma", "tma-stream"])
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 def test_sw2048_tma_x_sweep_with_revert(dtype, variant):
+    if variant == XVAR_TMA_STREAM and dtype == "float32":
+        pytest.skip("the streaming x geometry is fp64 shallow water only")
     r = _recipe("sw2048", "shallow_water2d", (2048, 2048), "radial_dam_break", dtype,
                 "reflective", "mc", 3, speed=("scale", 0.5))
     att, used = _run_both(r, variant)
-    assert used == (XVAR_TMA if variant is None else variant)
+    auto = XVAR_TMA_ADAPT if dtype == "float64" else XVAR_TMA
+    assert used == (auto if variant is None else variant)
     assert not att[0].accepted and att[1].accepted
 
 
@@ -100,15 +104,16 @@ def test_sw8192_north_star_tma_x_sweep():
     r = _recipe("sw8192", "shallow_water2d", (8192, 8192), "radial_dam_break", "float64",
                 "reflective", "mc", 3, speed=("scale", 0.5))
     att, used = _run_both(r)
-    assert used == XVAR_TMA
+    assert used == XVAR_TMA_ADAPT
     assert not att[0].accepted
 
 
-def test_sw8192_hump_active_flow_fp64():
+@pytest.mark.parametrize("variant", [None, XVAR_TMA_STREAM], ids=["auto", "tma-stream"])
+def test_sw8192_hump_active_flow_fp64(variant):
     # flow in every cell: the FastArith second pass is exercised in the far field
     r = _recipe("hump", "shallow_water2d", (4096, 4096), "gaussian_hump", "float64",
                 "periodic", "mc", 4)
-    _run_both(r)
+    _run_both(r, variant)
 
 
 def test_c3_vc_acoustics_256cube_superbee():
@@ -121,7 +126,7 @@ def test_c4_sw16384_two_steps():
     r = _recipe("c4", "shallow_water2d", (16384, 16384), "radial_dam_break", "float64",
                 "reflective", "mc", 2)
     _, used = _run_both(r)
-    assert used == XVAR_TMA
+    assert used == XVAR_TMA_ADAPT
 
 
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
