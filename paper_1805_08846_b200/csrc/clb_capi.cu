@@ -309,7 +309,7 @@ clb::GenericArgs sweep_geometry(clb_ctx* h, int axis, int src, int dst, int xs =
   }
   // contig stages are 64 (legacy: 48) bytes of a row: segment starts stay aligned
   const int64_t align =
-      (axis == 0 && g.contig == 2) ? (CLB_X_LEGACY ? 48 : clb::x_row_bytes(h->M, g.xs)) / h->itemsize
+      (axis == 0 && g.contig == 2) ? (CLB_X_LEGACY ? 48 : clb::x_stage_bytes(h->M, g.xs)) / h->itemsize
                                    : 1;
   static const int64_t min_seg = [] {
     const char* e = getenv("CLB_MIN_SEG");

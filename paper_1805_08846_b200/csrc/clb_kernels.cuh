@@ -79,6 +79,9 @@ constexpr int kXRows = CLB_X_ROWS;
 #ifndef CLB_XS_MINB
 #define CLB_XS_MINB 5
 #endif
+#ifndef CLB_XS_SUB
+#define CLB_XS_SUB 1    // boxes side by side along x per stage of the streaming twin
+#endif
 template <int XS> constexpr int x_rows() { return XS ? CLB_XS_ROWS : kXRows; }
 template <bool CONTIG, int XS = 0> constexpr int threads_of() {
   return ((CONTIG && !CLB_X_LEGACY) ? x_rows<XS>() : kConsumers) +
@@ -900,11 +903,18 @@ __host__ __device__ constexpr int x_row_bytes(int m, int xs = 0) {
 template <typename T, class S> constexpr bool has_xs() {
   return sizeof(T) == 8 && S::M == 3 && S::NW >= 3 && !CLB_X_LEGACY;
 }
+// cells per stage (x_row_bytes per box, SUB boxes side by side)
+__host__ __device__ constexpr int x_stage_bytes(int m, int xs = 0) {
+  return x_row_bytes(m, xs) * (xs ? CLB_XS_SUB : 1);
+}
 template <typename T, class S, int XS = 0> struct XGeom {
   static constexpr int ROWS = x_rows<XS>();             // rows (consumer threads) per CTA
-  static constexpr int ROW = x_row_bytes(S::M, XS);     // bytes per row per state
-  static constexpr int NC = ROW / (int)sizeof(T);
-  static constexpr int SBYTES = ROWS * ROW;             // one state of a stage
+  static constexpr int ROW = x_row_bytes(S::M, XS);     // bytes per row per state and box
+  static constexpr int SUB = XS ? CLB_XS_SUB : 1;       // boxes per state and stage
+  static constexpr int NCS = ROW / (int)sizeof(T);      // cells per box
+  static constexpr int NC = SUB * NCS;                  // cells per stage
+  static constexpr int SUBB = ROWS * ROW;               // one box
+  static constexpr int SBYTES = SUB * SUBB;             // one state of a stage
   static constexpr int BYTES = S::M * SBYTES;
   // as many stages as the ring budget holds (in-place outputs need >= 3)
   // the resident CTAs' share of the 228 KB (less static + reserved memory)
@@ -948,7 +958,10 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
     const int cx = a.tx0 + lo - NC + k * NC;
 #pragma unroll
     for (int q = 0; q < M; ++q)
-      tma_load_4d(ring + s * G::BYTES + q * G::SBYTES, map_ld, cx, cy, cz, q, &full[s]);
+#pragma unroll
+      for (int u = 0; u < G::SUB; ++u)
+        tma_load_4d(ring + s * G::BYTES + q * G::SBYTES + u * G::SUBB, map_ld, cx + u * G::NCS,
+                    cy, cz, q, &full[s]);
   };
   if (!kInlineX && warp == G::ROWS / 32) {
     if (lane == 0)
@@ -977,7 +990,9 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
   // (128-byte rows, 128-byte swizzle: chunk ^= t & 7)
   const int xr = G::ROW == 128 ? (t & 7) << 4
                  : G::ROW == 64 ? ((t >> 1) & 3) << 4 : ((t >> 2) & 1) << 4;
-  auto cell_off = [&](int c) { return rowb + ((c * isz) ^ xr); };
+  auto cell_off = [&](int c) {
+    return (c / G::NCS) * G::SUBB + rowb + (((c % G::NCS) * isz) ^ xr);
+  };
 
   March<T, S, LIM, LIT, D> mr;
   mr.smax = T(0);
@@ -1036,7 +1051,10 @@ __device__ __forceinline__ void segment_pass_x(const SweepArgs<T>& a, const Live
       const int cx = a.tx0 + lo + (k - 1) * NC;
       if (!CLB_DIAG_NOSTORE) {  // timing experiments only: outputs discarded
 #pragma unroll
-        for (int q = 0; q < M; ++q) tma_store_4d(map_st, st + q * G::SBYTES, cx, cy, cz, q);
+        for (int q = 0; q < M; ++q)
+#pragma unroll
+          for (int u = 0; u < G::SUB; ++u)
+            tma_store_4d(map_st, st + q * G::SBYTES + u * G::SUBB, cx + u * G::NCS, cy, cz, q);
       }
       bulk_commit();
       // every stage before k is consumed; the store of k-1 has read its slot

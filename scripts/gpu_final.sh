@@ -14,9 +14,10 @@ for w in c1 c2 c3 c5 c5f32 sw8192 sw8192hump sw8192f32 c4lake; do b $w; done
 timeout 600 python bench.py --workload c5 --steps 10 --warmup 3 > $O/bench_c5_full.json 2> $O/bench_c5_full.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
   --log-file $O/launches_c4.csv python bench.py --steps 4 --warmup 3 --no-cpu > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel" -s 6 -c 2 \
+# fp64 SW: three sweep_kernel launches per attempt (the x geometry pair + y)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel" -s 9 -c 3 \
   -o $O/prof_c4 python bench.py --workload c4 --steps 2 --warmup 3 --no-cpu > $O/ncu_c4.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel" -s 6 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel" -s 9 -c 3 \
   -o $O/prof_hump python bench.py --workload sw8192hump --steps 2 --warmup 3 --no-cpu > $O/ncu_hump.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel" -s 9 -c 3 \
   -o $O/prof_c5 python bench.py --workload c5 --steps 2 --warmup 3 --no-cpu > $O/ncu_c5.log 2>&1
