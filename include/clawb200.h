@@ -124,6 +124,11 @@ enum {
 int clb_set_x_variant(clb_handle h, int variant);
 /* The variant the next x sweep of this handle launches (1 .. 5). */
 int clb_x_variant(clb_handle h, int32_t *variant);
+/* The geometry pair's selector (CLB_XVAR_TMA_ADAPT only; CLB_EUNSUPPORTED
+ * otherwise): the warp groups the strided sweeps computed (not skipped) since
+ * the last x sweep, and the count below which the next x sweep runs the
+ * streaming twin.  Synchronises the handle's stream (tests / diagnostics). */
+int clb_x_activity(clb_handle h, uint64_t *computed, uint64_t *threshold);
 
 /* Interior transfer, frame-payload order: state-major, then z, y, x (x
  * fastest), ghost cells excluded; nbytes must equal m*prod(cells)*itemsize.

@@ -36,6 +36,7 @@ EXPORTS = (
     "clb_enable_timing", "clb_timing", "clb_host_alloc", "clb_host_free", "clb_memory_info",
     "clb_selftest_arith", "clb_run_batch", "clb_frame_size", "clb_write_frame",
     "clb_sweep_segments", "clb_sweep_async_range", "clb_set_x_variant", "clb_x_variant",
+    "clb_x_activity",
     "clb_register_device_solver", "clb_sweep_args_size", "clb_nccl_unique_id",
     "clb_attach_comm", "clb_halo_exchange", "clb_results_allreduce",
 )
@@ -122,6 +123,8 @@ def lib():
         "clb_halo_exchange": (_int, [_vp, _int]),
         "clb_results_allreduce": (_int, [_vp]),
         "clb_x_variant": (_int, [_vp, ctypes.POINTER(_i32)]),
+        "clb_x_activity": (_int, [_vp, ctypes.POINTER(ctypes.c_uint64),
+                                  ctypes.POINTER(ctypes.c_uint64)]),
         "clb_upload": (_int, [_vp, _int, _vp, _sz]),
         "clb_download": (_int, [_vp, _int, _vp, _sz]),
         "clb_upload_padded": (_int, [_vp, _int, _vp, _sz]),
@@ -268,6 +271,14 @@ class DeviceGrid:
         v = _i32(0)
         _check(lib().clb_x_variant(self.handle, ctypes.byref(v)), self.handle)
         return int(v.value)
+
+    def x_activity(self) -> tuple[int, int]:
+        """(computed strided warp groups since the last x sweep, threshold):
+        the geometry pair runs its streaming twin next while computed <
+        threshold (XVAR_TMA_ADAPT handles only)."""
+        c, t = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        _check(lib().clb_x_activity(self.handle, ctypes.byref(c), ctypes.byref(t)), self.handle)
+        return int(c.value), int(t.value)
 
     def attach_comm(self, uid: bytes, nranks: int, rank: int, lo_nbr, hi_nbr):
         """Device-resident slab exchange over NCCL (clb_attach_comm)."""

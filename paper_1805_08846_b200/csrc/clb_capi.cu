@@ -934,6 +934,19 @@ int clb_x_variant(clb_handle h, int32_t* variant) {
   return CLB_OK;
 }
 
+int clb_x_activity(clb_handle h, uint64_t* computed, uint64_t* threshold) {
+  if (!h || !computed || !threshold) return fail(h, CLB_EINVAL, "null argument");
+  if (x_mode(h) != CLB_XVAR_TMA_ADAPT)
+    return fail(h, CLB_EUNSUPPORTED, "the handle does not run the x geometry pair");
+  cudaSetDevice(h->d.device);
+  unsigned long long v = 0;
+  CLB_CUDA(h, cudaMemcpyAsync(&v, h->d_act, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
+  CLB_CUDA(h, cudaStreamSynchronize(h->stream));
+  *computed = (uint64_t)v;
+  *threshold = (uint64_t)h->xs_thresh;
+  return CLB_OK;
+}
+
 // Pitched 3-D copy of one state between host (dense) and device (pitched).
 static cudaError_t copy_state(clb_ctx* h, int buf, int k, void* host, bool padded, bool to_dev) {
   const int64_t isz = h->itemsize;

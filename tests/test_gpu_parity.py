@@ -195,6 +195,31 @@ def test_streaming_x_geometry_matches_oracle(shape, bc, limiter, variant):
         assert sim.grid.interior().tobytes() == O.interior(osim.grid).tobytes()
 
 
+@pytest.mark.parametrize("profile,expect_stream", [("radial_dam_break", True),
+                                                   ("gaussian_hump", False)],
+                         ids=["dam-break-quiescent", "hump-active"])
+def test_geometry_pair_selects_by_activity(profile, expect_stream):
+    """The pair's selector after an attempt holds the y sweep's computed warp
+    groups: far below the threshold for an early dam break (most groups
+    skipped, so the next x sweep runs the streaming twin), above it for flow
+    active everywhere; results stay bitwise equal to the oracle."""
+    r = _recipe("shallow_water2d", (2048, 2048), profile, {}, "float64", "reflective", "mc",
+                steps=2)
+    osim, _ = cases.oracle_sim(r)
+    oatt = cases.drive(osim, r)
+    sim, _ = cases.product_sim(r)
+    with sim:
+        assert sim.device_grid.x_variant() == XVAR_TMA_ADAPT
+        computed, thresh = sim.device_grid.x_activity()
+        assert computed == 2**64 - 1          # before any strided sweep: default twin
+        att = cases.drive(sim, r)             # the device controller's graph
+        computed, thresh = sim.device_grid.x_activity()
+        assert thresh == int(0.08 * (2048 // 32) * ((2048 + 2) // 3))
+        assert (computed < thresh) == expect_stream, (computed, thresh)
+        assert cases.attempts_hex(att) == cases.attempts_hex(oatt)
+        assert sim.grid.interior().tobytes() == O.interior(osim.grid).tobytes()
+
+
 def test_streaming_x_geometry_is_fp64_shallow_water_only():
     r = _recipe("acoustics2d", (64, 40), "gaussian_pressure", {"width": 0.15}, "float64",
                 "periodic", "mc", steps=1)
@@ -203,6 +228,8 @@ def test_streaming_x_geometry_is_fp64_shallow_water_only():
         for v in (XVAR_TMA_STREAM, XVAR_TMA_ADAPT):
             with pytest.raises(Exception, match="fp64 2-D shallow water"):
                 sim.device_grid.set_x_variant(v)
+        with pytest.raises(Exception, match="geometry pair"):
+            sim.device_grid.x_activity()
     r = _recipe("shallow_water2d", (64, 40), "radial_dam_break", {}, "float32", "periodic", "mc",
                 steps=1)
     sim, _ = cases.product_sim(r)
