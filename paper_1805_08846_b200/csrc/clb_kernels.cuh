@@ -83,6 +83,11 @@ constexpr int kXRows = CLB_X_ROWS;
 #define CLB_XS_SUB 1    // boxes side by side along x per stage of the streaming twin
 #endif
 template <int XS> constexpr int x_rows() { return XS ? CLB_XS_ROWS : kXRows; }
+// the solvers whose x sweep has a streaming twin (XS = 1): fp64 shallow
+// water; only their strided sweeps count computed groups (SweepArgs::act)
+template <typename T, class S> __host__ __device__ constexpr bool has_xs() {
+  return sizeof(T) == 8 && S::M == 3 && S::NW >= 3 && !CLB_X_LEGACY;
+}
 template <bool CONTIG, int XS = 0> constexpr int threads_of() {
   return ((CONTIG && !CLB_X_LEGACY) ? x_rows<XS>() : kConsumers) +
          (inline_producer<CONTIG>() ? 0 : 32);
@@ -818,7 +823,7 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
           }
           mr.uni = false;
         }
-        ++nact;
+        if constexpr (has_xs<T, S>()) ++nact;
         T o[M];
         bool v;
         v = r0 < ncell;
@@ -856,7 +861,8 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
     if (last > flushed) flush(last);
     if (t == 0) bulk_wait<0>();
   }
-  if (!CONTIG && a.act && lane == 0 && nact) atomicAdd(a.act, (unsigned long long)nact);
+  if constexpr (!CONTIG && has_xs<T, S>())
+    if (a.act && lane == 0 && nact) atomicAdd(a.act, (unsigned long long)nact);
   smax = mr.smax;
   fin = mr.fin;
   bad = mr.bad && active;
@@ -898,10 +904,6 @@ __device__ __forceinline__ void segment_pass(const SweepArgs<T>& a, const Live<T
 // box row bytes of the x stages (host side: clb_capi.cu make_tensor_map)
 __host__ __device__ constexpr int x_row_bytes(int m, int xs = 0) {
   return xs ? CLB_XS_ROW : (m >= 4 ? CLB_X_ROW4 : CLB_X_ROW);
-}
-// the x geometries with a streaming twin (XS = 1): fp64 shallow water
-template <typename T, class S> constexpr bool has_xs() {
-  return sizeof(T) == 8 && S::M == 3 && S::NW >= 3 && !CLB_X_LEGACY;
 }
 // cells per stage (x_row_bytes per box, SUB boxes side by side)
 __host__ __device__ constexpr int x_stage_bytes(int m, int xs = 0) {
